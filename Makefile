@@ -1,0 +1,26 @@
+# Build the C-ABI library in-tree (it travels to the GPU box with the snapshot).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2206_01861_b200
+SRC := $(PKG)/csrc/zq_quant.cu $(PKG)/csrc/zq_gemm.cu
+HDR := include/zq_b200.h $(PKG)/csrc/zq_common.cuh
+# -fmad=false: no FMA contraction anywhere (bit-exact numpy arithmetic); the
+# exactness-critical ops additionally use explicit _rn intrinsics.
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Iinclude \
+           -Xptxas -v --expt-relaxed-constexpr
+
+LIB := $(PKG)/libzq_b200.so
+
+all: $(LIB)
+
+$(PKG)/build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(PKG)/build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(PKG)/build/$*.ptxas.log || (cat $(PKG)/build/$*.ptxas.log; false)
+
+$(LIB): $(PKG)/build/zq_quant.o $(PKG)/build/zq_gemm.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lrt -ldl -lpthread
+
+clean:
+	rm -rf $(PKG)/build $(LIB)
+
+.PHONY: all clean

@@ -1,0 +1,142 @@
+/*
+ * zq_b200.h — C ABI of the B200-native ZeroQuant hot path (libzq_b200.so).
+ *
+ * Every entry point takes caller-owned DEVICE buffers (plain pointers + sizes),
+ * enqueues asynchronously on `stream` (a cudaStream_t passed as void*), and
+ * returns a status code.  No torch types cross this boundary.
+ *
+ * Status codes map onto the reference's error taxonomy
+ * (pkg/src/lowbit/errors.py:8-13):
+ *   ZQ_OK            0
+ *   ZQ_ERR_USAGE     1  -> lowbit.errors.UsageError
+ *   ZQ_ERR_SHAPE     2  -> lowbit.errors.ShapeError
+ *   ZQ_ERR_CUDA      3  -> RuntimeError (launch / driver failure)
+ *   ZQ_ERR_UNSUPPORTED 4 -> UsageError (shape outside what the kernel handles)
+ * Non-finite inputs are reported through `nonfinite_flag` (device int32,
+ * caller-zeroed; set to 1 by the kernel), which the host raises as ValueError
+ * (pkg/src/lowbit/quant.py:109-110, :247-248, :265-266).
+ *
+ * Layouts (row-major, C order):
+ *   activations  f32 [rows, cols], row stride ld (elements)
+ *   int8 payload [rows, ld_q] with ld_q % 16 == 0 and zero padding past cols
+ *   weights      int8 [N, ld_w] output-major (igemm.py:66-80 reads w row j for
+ *                output channel j); W4 packed: uint8 [N, ld_w/2], element 2k in
+ *                the low nibble of byte k (two's complement)
+ *   row scales   f32 [N]   (QuantizedMatrix.row_scales(), quant.py:165-170)
+ *   token scales f32 [rows]
+ */
+#ifndef ZQ_B200_H_
+#define ZQ_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZQ_OK 0
+#define ZQ_ERR_USAGE 1
+#define ZQ_ERR_SHAPE 2
+#define ZQ_ERR_CUDA 3
+#define ZQ_ERR_UNSUPPORTED 4
+
+/* output element types of the dequant epilogue */
+#define ZQ_OUT_F32 0
+#define ZQ_OUT_F16 1
+#define ZQ_OUT_BF16 2
+
+/* library version / build identification (for the loaded-.so audit) */
+const char* zq_version(void);
+
+/* Last error message of the calling thread (static storage). */
+const char* zq_last_error(void);
+
+/* Replaces quant.quantize_activation_tokenwise (pkg/src/lowbit/quant.py:258-269):
+ * per-row scale s = f32(max|x| / qmax) (0 -> 1.0), q = clamp(RHAFZ(x/s)). */
+int zq_quantize_tokenwise(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int bits,
+                          int8_t* q, int64_t ld_q, float* token_scales, int32_t* nonfinite_flag,
+                          void* stream);
+
+/* Replaces quant.quantize_activation_static (pkg/src/lowbit/quant.py:272-281) and
+ * quant.quantize_array (quant.py:103-113): q = clamp(RHAFZ(f64(x) / scale)). */
+int zq_quantize_static(const float* x, int64_t rows, int64_t cols, int64_t ld_x, double scale,
+                       int bits, int8_t* q, int64_t ld_q, int32_t* nonfinite_flag, void* stream);
+
+/* Replaces quant.quantize_weight_groupwise (pkg/src/lowbit/quant.py:236-255):
+ * contiguous row groups (group_layout_for, quant.py:211-219), one f32 scale per
+ * group, also writes the expanded per-row scale vector (QuantizedMatrix.row_scales).
+ * `packed4` (nullable, bits==4 only) additionally receives the packed INT4 payload
+ * [rows, ld_q/2]. */
+int zq_quantize_weight_groupwise(const float* w, int64_t rows, int64_t cols, int64_t groups,
+                                 int bits, int8_t* q, int64_t ld_q, float* group_scales,
+                                 float* row_scales, uint8_t* packed4, int32_t* nonfinite_flag,
+                                 void* stream);
+
+/* Packs an int8 payload with values in [-7, 7] into two's-complement nibbles. */
+int zq_pack_int4(const int8_t* q, int64_t rows, int64_t ld_q, uint8_t* packed, void* stream);
+
+/* Replaces igemm.layer_norm_quantize (pkg/src/lowbit/igemm.py:150-157) over
+ * tensor.layer_norm (pkg/src/lowbit/tensor.py:59-73), optionally fused with the
+ * residual add that feeds it in block_forward (transformer.py:477, :486):
+ * y = LN(x [+ residual]) with numpy's pairwise f32 reductions; writes the float
+ * LN output (nullable) and its token-wise quantization. */
+int zq_layer_norm_quantize(const float* x, const float* residual, const float* gamma,
+                           const float* beta, int64_t rows, int64_t cols, float eps, int bits,
+                           float* ln_out, int8_t* q, int64_t ld_q, float* token_scales,
+                           int32_t* nonfinite_flag, void* stream);
+
+/* Replaces igemm.gelu_quantize (pkg/src/lowbit/igemm.py:160-161) over tensor.gelu
+ * (pkg/src/lowbit/tensor.py:76-83): exact-erf GeLU in f64 rounded once to f32,
+ * then token-wise quantization.  gelu_out (nullable) receives the f32 GeLU. */
+int zq_gelu_quantize(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int bits,
+                     float* gelu_out, int8_t* q, int64_t ld_q, float* token_scales,
+                     int32_t* nonfinite_flag, void* stream);
+
+/* Replaces igemm.igemm (pkg/src/lowbit/igemm.py:66-80): exact int32
+ * acc[M,N] = xq[M,K] . wq[N,K]^T on tcgen05 kind::i8 tensor cores.
+ * w_bits: 8 (int8 payload, ld_w bytes per row) or 4 (packed payload, ld_w/2 bytes per row). */
+int zq_igemm_s32(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
+                 int64_t M, int64_t N, int64_t K, int32_t* acc, int64_t ld_acc, void* stream);
+
+/* Replaces igemm.quantized_linear for Dynamic/Static activations
+ * (pkg/src/lowbit/igemm.py:115-139) after the activation quantizer: the fused
+ * igemm + dequant_epilogue (igemm.py:83-112):
+ *   out = ((f32(acc) * s_tok[i]) * s_w[j]) + bias[j]
+ * token_scales == NULL selects the static path with `static_scale` (f32-rounded,
+ * igemm.py:98-99).  bias nullable.  out_type: ZQ_OUT_F32/F16/BF16 (RN cast of
+ * the exact f32 value). */
+int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float static_scale,
+              const void* wq, int64_t ld_w, int w_bits, const float* w_row_scales,
+              const float* bias, int64_t M, int64_t N, int64_t K, void* out, int64_t ld_out,
+              int out_type, void* stream);
+
+/* Standalone dequant epilogue over an int32 accumulator (igemm.py:83-112); used
+ * after the tensor-parallel int32 all-reduce. */
+int zq_dequant_epilogue(const int32_t* acc, int64_t ld_acc, const float* token_scales,
+                        float static_scale, const float* w_row_scales, const float* bias,
+                        int64_t M, int64_t N, void* out, int64_t ld_out, int out_type,
+                        void* stream);
+
+/* Replaces igemm.quantized_linear(FullAct) (pkg/src/lowbit/igemm.py:127-130):
+ * weight-only path, out = matmul(x, dequant(w).T) + bias with the reference's
+ * sequential f32 accumulation order (tensor.py:37-56). */
+int zq_linear_full(const float* x, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
+                   const float* w_row_scales, const float* bias, int64_t M, int64_t N,
+                   int64_t K, float* out, int64_t ld_out, void* stream);
+
+/* Row absmax (f32 bit patterns, non-negative) for the tensor-parallel token-scale
+ * all-reduce: amax[i] = max_j |x[i, j]|. */
+int zq_row_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x, float* amax,
+                  int32_t* nonfinite_flag, void* stream);
+
+/* Token-wise quantization with externally supplied per-row absmax (the
+ * all-reduced global max in the row-parallel TP path). */
+int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x,
+                            const float* amax, int bits, int8_t* q, int64_t ld_q,
+                            float* token_scales, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZQ_B200_H_ */

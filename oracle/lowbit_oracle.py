@@ -484,3 +484,59 @@ def unpack_int4(packed: np.ndarray) -> np.ndarray:
     out[..., 0::2] = lo
     out[..., 1::2] = hi
     return out
+
+
+# ---------------------------------------------------------------------------
+# scipy.special.erf provenance (the f64 erf inside tensor.gelu, tensor.py:15,83)
+# ---------------------------------------------------------------------------
+# scipy 1.18's real erf is the Cephes ndtr.c algorithm; restated here (and in
+# the GPU kernel, csrc/zq_quant.cu cephes_erf) so that the GeLU's f64 value —
+# whose low bits survive the 1 + erf(x) cancellation for x << 0 — is pinned to
+# a written-down algorithm.  tests/test_oracle_golden.py checks it equals scipy.
+_ERF_T = [9.60497373987051638749E0, 9.00260197203842689217E1, 2.23200534594684319226E3,
+          7.00332514112805075473E3, 5.55923013010394962768E4]
+_ERF_U = [3.35617141647503099647E1, 5.21357949780152679795E2, 4.59432382970980127987E3,
+          2.26290000613890934246E4, 4.92673942608635921086E4]
+_ERF_P = [2.46196981473530512524E-10, 5.64189564831068821977E-1, 7.46321056442269912687E0,
+          4.86371970985681366614E1, 1.96520832956077098242E2, 5.26445194995477358631E2,
+          9.34528527171957607540E2, 1.02755188689515710272E3, 5.57535335369399327526E2]
+_ERF_Q = [1.32281951154744992508E1, 8.67072140885989742329E1, 3.54937778887819891062E2,
+          9.75708501743205489753E2, 1.82390916687909736289E3, 2.24633760818710981792E3,
+          1.65666309194161350182E3, 5.57535340817727675546E2]
+_ERF_R = [5.64189583547755073984E-1, 1.27536670759978104416E0, 5.01905042251180477414E0,
+          6.16021097993053585195E0, 7.40974269950448939160E0, 2.97886665372100240670E0]
+_ERF_S = [2.26052863220117276590E0, 9.39603524938001434673E0, 1.20489539808096656605E1,
+          1.70814450747565897222E1, 9.60896809063285878198E0, 3.36907645100081516050E0]
+_MAXLOG = 7.09782712893383996843E2
+
+
+def _polevl(x, c, n):
+    a = c[0]
+    for i in range(1, n + 1):
+        a = a * x + c[i]
+    return a
+
+
+def _p1evl(x, c, n):
+    a = x + c[0]
+    for i in range(1, n):
+        a = a * x + c[i]
+    return a
+
+
+def cephes_erf(x: float) -> float:
+    """Scalar Cephes erf in IEEE double (Python floats), op order as ndtr.c."""
+    if x < 0.0:
+        return -cephes_erf(-x)
+    if x <= 1.0:
+        z = x * x
+        return x * _polevl(z, _ERF_T, 4) / _p1evl(z, _ERF_U, 5)
+    z = -x * x
+    if z < -_MAXLOG:
+        return 1.0
+    e = math.exp(z)
+    if x < 8.0:
+        p, q = _polevl(x, _ERF_P, 8), _p1evl(x, _ERF_Q, 8)
+    else:
+        p, q = _polevl(x, _ERF_R, 5), _p1evl(x, _ERF_S, 6)
+    return 1.0 - (e * p) / q

@@ -1,0 +1,266 @@
+// Shared helpers for the sm_100a kernels: status codes, thread-local error text,
+// exact quantization arithmetic, and thin inline-PTX wrappers (mbarrier, TMA,
+// tcgen05) used by the GEMM.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "zq_b200.h"
+
+namespace zq {
+
+// ---------------------------------------------------------------------------
+// host-side error reporting
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+
+#define ZQ_CHECK_ARG(cond, code, ...)     \
+  do {                                    \
+    if (!(cond)) {                        \
+      ::zq::set_error(__VA_ARGS__);       \
+      return (code);                      \
+    }                                     \
+  } while (0)
+
+#define ZQ_LAUNCH_CHECK(what)                                                  \
+  do {                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                       \
+    if (e_ != cudaSuccess) {                                                   \
+      ::zq::set_error("%s: %s", (what), cudaGetErrorString(e_));               \
+      return ZQ_ERR_CUDA;                                                      \
+    }                                                                          \
+  } while (0)
+
+inline int qmax_of(int bits) { return (1 << (bits - 1)) - 1; }
+inline bool bits_ok(int bits) { return bits == 4 || bits == 8; }
+
+// ---------------------------------------------------------------------------
+// device: exact ZeroQuant rounding (pkg/src/lowbit/quant.py:98-113, :229-233)
+// ---------------------------------------------------------------------------
+
+// Scale from a row max (quant.py:222-226): f32(f64(maxabs) / qmax), 0 -> 1.0.
+// f64 division and the single cvt.rn.f32.f64 are exactly numpy's arithmetic.
+__device__ __forceinline__ float scale_from_absmax(float amax, int qm) {
+  if (amax == 0.0f) return 1.0f;
+  return __double2float_rn(__ddiv_rn((double)amax, (double)qm));
+}
+
+// q = clamp(sign(x) * floor(|x|/s + 1/2), +-qm) for f32 x and f32 s > 0.
+// The reference divides in f64; for f32 operands its result equals exact
+// round-half-away of the rational |x|/s (the f64 quotient cannot cross a
+// half-integer it is not exactly on).  We estimate k from an f32 quotient and
+// fix it with an exact f64 boundary test: (k -+ 1/2) * s is exact in f64
+// (24-bit s times a <=10-bit half-integer).
+__device__ __forceinline__ int quantize_exact(float x, float s, int qm) {
+  float ax = fabsf(x);
+  float r = fminf(__fdiv_rn(ax, s), 512.0f);
+  int k = __float2int_rd(__fadd_rn(r, 0.5f));
+  double axd = (double)ax, sd = (double)s;
+  if (__dmul_rn((double)k - 0.5, sd) > axd) {
+    k -= 1;
+  } else if (__dmul_rn((double)k + 0.5, sd) <= axd) {
+    k += 1;
+  }
+  k = min(k, qm);
+  return x < 0.0f ? -k : k;
+}
+
+// Static path with an arbitrary f64 scale: numpy's exact op sequence
+// (f64 divide, f64 add 0.5, floor, clip).
+__device__ __forceinline__ int quantize_f64(float x, double s, int qm) {
+  double v = __ddiv_rn((double)x, s);
+  double a = floor(__dadd_rn(fabs(v), 0.5));
+  a = fmin(a, (double)qm);
+  int k = (int)a;
+  return v < 0.0 ? -k : k;
+}
+
+__device__ __forceinline__ bool is_finite_f(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide max of a non-negative float (as its u32 bit pattern — monotone for
+// non-negative floats, NaN never reaches here because the finite flag is raised
+// separately).  `red` must hold >= 32 words.
+__device__ __forceinline__ float block_max_nonneg(float v, uint32_t* red) {
+  uint32_t b = warp_max(__float_as_uint(v));
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = b;
+  __syncthreads();
+  int nw = (blockDim.x + 31) >> 5;
+  b = (threadIdx.x < nw) ? red[threadIdx.x] : 0u;
+  if (w == 0) {
+    b = warp_max(b);
+    if (l == 0) red[0] = b;
+  }
+  __syncthreads();
+  return __uint_as_float(red[0]);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// smem -> global tensor store (bulk async group), clipped to the tensor bounds.
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   tmap),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- tcgen05 ---------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32, one elected thread.
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor for a K-major, SWIZZLE_128B operand tile whose
+// rows are 128 bytes and whose 8-row core groups are 1024 bytes apart
+// (SM100 UMMA descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+// version=1 [46,48), base_offset [49,52), layout SWIZZLE_128B=2 [61,64)).
+__device__ __forceinline__ uint64_t make_sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(16u >> 4) << 16;   // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32; // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::i8, A/B signed int8, K-major both, D = s32.
+__host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
+  return (2u << 4)                       // c_format = S32
+         | (1u << 7)                     // a_format = INT8 (signed)
+         | (1u << 10)                    // b_format = INT8 (signed)
+         | ((uint32_t)(N >> 3) << 17)    // N >> 3
+         | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+
+}  // namespace zq

@@ -1,0 +1,685 @@
+// K6/K7/K8: W8A8 / W4A8 integer GEMM on sm_100a tensor cores (tcgen05 kind::i8)
+// with the fused ZeroQuant dequant epilogue.
+//
+//   acc[i, j] = sum_p xq[i, p] * wq[j, p]            igemm.py:66-80 (exact int32)
+//   out[i, j] = ((f32(acc) * s_tok[i]) * s_w[j]) + b[j]   igemm.py:83-112
+//
+// Persistent, warp-specialised kernel, one CTA per SM:
+//   warp 0      TMA producer (one elected lane): A/B K-blocks -> smem ring
+//   warp 1      TMEM allocator + MMA issuer (one lane): tcgen05.mma kind::i8
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> dequant -> global
+//   warps 6..9  (W4 only) INT4 -> INT8 unpack of the weight tile into the
+//               SWIZZLE_128B layout the MMA reads
+// Tiles: BLOCK_M = 128 token rows, BLOCK_N output channels (64/128/256),
+// BLOCK_K = 128 bytes (one 128B swizzle atom per row).  Accumulators are int32
+// in TMEM, double-buffered so the epilogue of tile t overlaps the MMAs of t+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "zq_common.cuh"
+
+namespace zq {
+
+constexpr int BLOCK_M = 128;
+constexpr int BLOCK_K = 128;
+constexpr int kNumEpiWarps = 8;
+
+enum OutKind { OUT_S32 = 0, OUT_F32 = 1, OUT_F16 = 2, OUT_BF16 = 3 };
+
+struct GemmParams {
+  int M, N, K;
+  int num_n_tiles, num_tiles, num_k_blocks;
+  void* out;
+  int64_t ld_out;
+  const float* token_scales;  // nullable -> static_scale
+  float static_scale;
+  const float* row_scales;    // per output channel (nullable for OUT_S32)
+  const float* bias;          // nullable
+  const uint8_t* w4;          // packed int4 weights (W4 path), row stride ld_w4 bytes
+  int64_t ld_w4;
+  int tma_out;                // output tensor map valid -> staged TMA stores
+};
+
+template <int BN, int W4>
+struct GemmCfg {
+  static constexpr int A_BYTES = BLOCK_M * BLOCK_K;
+  static constexpr int B_BYTES = BN * BLOCK_K;
+  static constexpr int P_BYTES = W4 ? BN * (BLOCK_K / 2) : 0;  // packed INT4 staging
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + P_BYTES;
+  static constexpr int STAGES = 192 * 1024 / STAGE_BYTES > 8 ? 8 : 192 * 1024 / STAGE_BYTES;
+  // per-epilogue-warp output staging: 32 rows x 32 columns x 4 B (f32/s32; f16 uses half)
+  static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 4;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered int32 accumulators
+  static constexpr int NUM_THREADS = (2 + kNumEpiWarps + (W4 ? 4 : 0)) * 32;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// Dequantize 32 accumulators of one output row (columns col0..col0+31) in the
+// reference's strict order ((f32(acc) * s_tok) * s_w) + bias and write them to
+// the warp's staging tile (row = lane) in the TMA swizzle layout:
+//   4-byte outputs: 128 B rows, SWIZZLE_128B: chunk c -> (c ^ (r & 7)) * 16
+//   2-byte outputs:  64 B rows, SWIZZLE_64B : chunk c -> (c ^ ((r >> 1) & 3)) * 16
+// Columns past N read scale/bias as 0 (their values are clipped by the TMA store).
+template <int KIND>
+__device__ __forceinline__ void epi_chunk_smem(const uint32_t (&r)[32], float s_tok,
+                                               const float* __restrict__ rs,
+                                               const float* __restrict__ bias, int col0, int N,
+                                               uint8_t* stage, int lane) {
+  if (KIND == OUT_S32) {
+    uint8_t* rowp = stage + lane * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+          make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+    return;
+  }
+  float f[32];
+  const bool full = col0 + 32 <= N;
+  if (full) {
+    const float4* sw4 = reinterpret_cast<const float4*>(rs + col0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 w = __ldg(sw4 + j);
+      f[4 * j + 0] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x);
+      f[4 * j + 1] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y);
+      f[4 * j + 2] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z);
+      f[4 * j + 3] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w);
+    }
+    if (bias != nullptr) {
+      const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b = __ldg(b4 + j);
+        f[4 * j + 0] = __fadd_rn(f[4 * j + 0], b.x);
+        f[4 * j + 1] = __fadd_rn(f[4 * j + 1], b.y);
+        f[4 * j + 2] = __fadd_rn(f[4 * j + 2], b.z);
+        f[4 * j + 3] = __fadd_rn(f[4 * j + 3], b.w);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int cc = col0 + j;
+      const float w = cc < N ? __ldg(rs + cc) : 0.0f;
+      f[j] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), s_tok), w);
+      if (bias != nullptr && cc < N) f[j] = __fadd_rn(f[j], __ldg(bias + cc));
+    }
+  }
+  if (KIND == OUT_F32) {
+    uint8_t* rowp = stage + lane * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<float4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+          make_float4(f[4 * c], f[4 * c + 1], f[4 * c + 2], f[4 * c + 3]);
+  } else {
+    uint32_t h[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (KIND == OUT_F16) {
+        __half2 t = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+        h[j] = *reinterpret_cast<uint32_t*>(&t);
+      } else {
+        __nv_bfloat162 t = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+        h[j] = *reinterpret_cast<uint32_t*>(&t);
+      }
+    }
+    uint8_t* rowp = stage + lane * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<uint4*>(rowp + ((c ^ ((lane >> 1) & 3)) << 4)) =
+          make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+  }
+}
+
+// Ragged edge (N tail or unaligned output): element-wise, guarded.
+template <int KIND>
+__device__ __forceinline__ void epi_chunk_slow(const uint32_t (&r)[32], float s_tok,
+                                            const float* __restrict__ rs,
+                                            const float* __restrict__ bias, void* out,
+                                            int64_t row_off, int col0, int N) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int c = col0 + j;
+    if (c < N) {
+      if (KIND == OUT_S32) {
+        reinterpret_cast<int32_t*>(out)[row_off + c] = (int)r[j];
+      } else {
+        float f = __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), s_tok), rs[c]);
+        if (bias) f = __fadd_rn(f, bias[c]);
+        if (KIND == OUT_F32) reinterpret_cast<float*>(out)[row_off + c] = f;
+        else if (KIND == OUT_F16) reinterpret_cast<__half*>(out)[row_off + c] = __float2half_rn(f);
+        else reinterpret_cast<__nv_bfloat16*>(out)[row_off + c] = __float2bfloat16_rn(f);
+      }
+    }
+  }
+}
+
+template <int BN, int KIND, int W4>
+__global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
+    zq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+  using Cfg = GemmCfg<BN, W4>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;                              // STAGES x [128 rows x 128 B]
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;      // STAGES x [BN rows x 128 B]
+  uint8_t* sP = smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES);  // W4: STAGES x [BN x 64 B]
+  uint8_t* sC = smem + STAGES * Cfg::STAGE_BYTES;  // epilogue staging (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + Cfg::EPI_BYTES);
+  uint64_t* full_bar = bars;                        // TMA (+unpack) -> MMA
+  uint64_t* empty_bar = bars + STAGES;              // MMA -> TMA (slot free)
+  uint64_t* tfull_bar = bars + 2 * STAGES;          // MMA -> epilogue (2)
+  uint64_t* tempty_bar = bars + 2 * STAGES + 2;     // epilogue -> MMA (2)
+  uint64_t* praw_bar = bars + 2 * STAGES + 4;       // W4: TMA packed weights landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    if (p.tma_out) prefetch_tmap(&tmC);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], W4 ? 1 + 4 : 1);  // W4: + one arrive per unpack warp
+      mbar_init(&empty_bar[s], 1);
+      if (W4) mbar_init(&praw_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], kNumEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nkb = p.num_k_blocks;
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    // whole warp walks the loop (keeps the warp converged for the final
+    // __syncthreads); lane 0 issues.
+    int stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
+      const int n0 = (tile % p.num_n_tiles) * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (lane == 0) {
+          if (W4) {
+            // packed weights -> staging (praw_bar); the unpack warps write the
+            // int8 tile and add 4 arrivals on full_bar
+            mbar_arrive_expect_tx(&praw_bar[stage], Cfg::P_BYTES);
+            tma_load_2d(sP + stage * Cfg::P_BYTES, &tmB, &praw_bar[stage], kb * (BLOCK_K / 2), n0);
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::A_BYTES);
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full_bar[stage], kb * BLOCK_K, m0);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full_bar[stage], kb * BLOCK_K, m0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full_bar[stage], kb * BLOCK_K, n0);
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = make_idesc_i8(BLOCK_M, BN);
+    int stage = 0, phase = 0, acc = 0, acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BLOCK_K / 32; ++k) {
+            mma_i8(d_tmem, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32),
+                   idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp < 2 + kNumEpiWarps) {
+    // ===================== epilogue =====================
+    // 8 warps: warp%4 selects the TMEM lane quarter (32 rows), (warp-2)/4 the
+    // half of the tile's columns.  Per 32x32 chunk: tcgen05.ld -> dequant in
+    // registers (thread = row) -> swizzled smem staging -> one TMA store per warp
+    // (coalesced, clipped at the M/N edges by the tensor map).
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int COLS = BN / 2;
+    uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
+    int acc = 0, acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
+      const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
+      const int row0 = m0 + quarter * 32;
+      const int row = row0 + lane;
+      float s_tok = p.static_scale;
+      if (KIND != OUT_S32 && p.token_scales != nullptr && row < p.M) s_tok = __ldg(p.token_scales + row);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
+#pragma unroll 1
+      for (int c = 0; c < COLS; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c, r);
+        tmem_ld_wait();
+        if (c + 32 == COLS) {
+          // accumulator fully read: hand the TMEM buffer back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        }
+        const int col0 = n0 + c;
+        if (row0 >= p.M || col0 >= p.N) continue;  // warp-uniform
+        if (p.tma_out) {
+          if (lane == 0) bulk_wait_read0();  // previous store finished reading stage_c
+          __syncwarp();
+          epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stage_c, col0, row0);
+            bulk_commit();
+          }
+        } else if (row < p.M) {
+          epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
+                               col0, p.N);
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  } else if (W4) {
+    // ===================== INT4 -> INT8 unpack (W4A8) =====================
+    // 4 warps.  Packed tile (BN rows x 64 B, K-major, unswizzled) -> int8 tile in
+    // the SWIZZLE_128B layout the MMA reads: row r, 16-byte chunk c (K elements
+    // 16c..16c+15) lives at r*128 + ((c ^ (r & 7)) * 16).  Nibble j of a packed
+    // 32-bit word is element j (two's complement), sign-extended with shifts.
+    const int ut = threadIdx.x - (2 + kNumEpiWarps) * 32;
+    int stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        mbar_wait(&praw_bar[stage], phase);
+        const uint8_t* src = sP + stage * Cfg::P_BYTES;
+        uint8_t* dst = sB + stage * Cfg::B_BYTES;
+#pragma unroll 4
+        for (int idx = ut; idx < BN * 8; idx += 128) {
+          const int r = idx >> 3, c = idx & 7;
+          const uint2 pk = *reinterpret_cast<const uint2*>(src + r * 64 + c * 8);
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t x = h ? pk.y : pk.x;
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              lo |= ((uint32_t)((int32_t)(x << (28 - 4 * e)) >> 28) & 0xFFu) << (8 * e);
+              hi |= ((uint32_t)((int32_t)(x << (12 - 4 * e)) >> 28) & 0xFFu) << (8 * e);
+            }
+            w[2 * h] = lo;
+            w[2 * h + 1] = hi;
+          }
+          *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) * 16)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to tcgen05
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// Standalone epilogue over an int32 accumulator (TP path) and the weight-only
+// FullAct GEMM (sequential f32 order, tensor.py:37-56).
+// ---------------------------------------------------------------------------
+__global__ void epilogue_kernel(const int32_t* __restrict__ acc, int64_t ld_acc,
+                                const float* __restrict__ ts, float static_scale,
+                                const float* __restrict__ rs, const float* __restrict__ bias,
+                                int64_t M, int64_t N, void* out, int64_t ld_out, int kind) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / N, c = i - r * N;
+    float s = ts ? ts[r] : static_scale;
+    float f = __fmul_rn(__fmul_rn(__int2float_rn(acc[r * ld_acc + c]), s), rs[c]);
+    if (bias) f = __fadd_rn(f, bias[c]);
+    int64_t o = r * ld_out + c;
+    if (kind == ZQ_OUT_F32) reinterpret_cast<float*>(out)[o] = f;
+    else if (kind == ZQ_OUT_F16) reinterpret_cast<__half*>(out)[o] = __float2half_rn(f);
+    else reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(f);
+  }
+}
+
+// 32x32 output tile per CTA (256 threads, 4 outputs each); K staged through smem
+// in chunks of 32; every output accumulates p = 0..K-1 in order with separately
+// rounded products and sums (no FMA), starting from +0.0.
+__global__ void __launch_bounds__(256) full_linear_kernel(
+    const float* __restrict__ x, int64_t ld_x, const int8_t* __restrict__ w8,
+    const uint8_t* __restrict__ w4, int64_t ld_w, const float* __restrict__ rs,
+    const float* __restrict__ bias, int64_t M, int64_t N, int64_t K, float* __restrict__ out,
+    int64_t ld_out) {
+  __shared__ float xs[32][33];
+  __shared__ float ws[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty 0..7
+  const int64_t m0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+    for (int i = ty; i < 32; i += 8) {
+      int64_t m = m0 + i, k = k0 + tx;
+      xs[i][tx] = (m < M && k < K) ? x[m * ld_x + k] : 0.0f;
+      int64_t n = n0 + i;
+      float wv = 0.0f;
+      if (n < N && k < K) {
+        int q;
+        if (w4) {
+          uint8_t b = w4[n * (ld_w / 2) + (k >> 1)];
+          int nib = (k & 1) ? (b >> 4) : (b & 0xF);
+          q = nib > 7 ? nib - 16 : nib;
+        } else {
+          q = w8[n * ld_w + k];
+        }
+        wv = __fmul_rn((float)q, rs[n]);  // QuantizedMatrix.dequantize, quant.py:172-174
+      }
+      ws[i][tx] = wv;
+    }
+    __syncthreads();
+    const int kk = (int)min((int64_t)32, K - k0);
+    for (int k = 0; k < kk; ++k) {
+      const float wv = ws[tx][k];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = __fadd_rn(acc[r], __fmul_rn(xs[ty + 8 * r][k], wv));
+    }
+    __syncthreads();
+  }
+  const int64_t n = n0 + tx;
+  if (n < N) {
+    float b = bias ? bias[n] : 0.0f;
+    for (int r = 0; r < 4; ++r) {
+      int64_t m = m0 + ty + 8 * r;
+      if (m < M) out[m * ld_out + n] = __fadd_rn(acc[r], b);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps, tile-shape selection, launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+static int make_tmap_u8(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols,
+                        int64_t ld_bytes, int box_cols, int box_rows, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld", (int)r,
+              (long long)rows, (long long)cols, (long long)ld_bytes);
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+static int g_num_sms = 0;
+
+template <int BN, int KIND, int W4>
+static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                         GemmParams p, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, W4>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zq_gemm_kernel<BN, KIND, W4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
+    attr = true;
+  }
+  int grid = p.num_tiles < g_num_sms ? p.num_tiles : g_num_sms;
+  zq_gemm_kernel<BN, KIND, W4><<<grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, tc, p);
+  ZQ_LAUNCH_CHECK("tcgen05 gemm launch");
+  return ZQ_OK;
+}
+
+template <int KIND, int W4>
+static int launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const CUtensorMap& tc, GemmParams p, cudaStream_t st) {
+  switch (bn) {
+    case 256: return launch_gemm_t<256, KIND, W4>(ta, tb, tc, p, st);
+    case 128: return launch_gemm_t<128, KIND, W4>(ta, tb, tc, p, st);
+    default: return launch_gemm_t<64, KIND, W4>(ta, tb, tc, p, st);
+  }
+}
+
+// Pick BLOCK_N: largest tile that still gives >= ~1 wave on 148 SMs; small-N
+// layers drop to 128/64 so the grid fills the machine.
+static int pick_bn(int64_t M, int64_t N) {
+  const int64_t mt = (M + BLOCK_M - 1) / BLOCK_M;
+  const int cands[3] = {256, 128, 64};
+  for (int i = 0; i < 3; ++i) {
+    int bn = cands[i];
+    int64_t tiles = mt * ((N + bn - 1) / bn);
+    if (tiles >= g_num_sms || bn == 64) {
+      if (bn > N && bn > 64) continue;
+      return bn;
+    }
+  }
+  return 64;
+}
+
+static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
+                       int64_t M, int64_t N, int64_t K, int kind, GemmParams p,
+                       cudaStream_t st) {
+  ZQ_CHECK_ARG(w_bits == 8 || w_bits == 4, ZQ_ERR_USAGE, "unsupported weight bit width %d", w_bits);
+  ZQ_CHECK_ARG(M >= 1 && N >= 1 && K >= 1, ZQ_ERR_SHAPE, "empty GEMM (%lld, %lld, %lld)",
+               (long long)M, (long long)N, (long long)K);
+  ZQ_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), ZQ_ERR_UNSUPPORTED,
+               "GEMM dimension too large");
+  ZQ_CHECK_ARG(ld_x >= K && ld_x % 16 == 0, ZQ_ERR_USAGE, "activation row stride %lld must be >= K and a multiple of 16",
+               (long long)ld_x);
+  ZQ_CHECK_ARG(ld_w >= K && ld_w % 16 == 0 && (w_bits == 8 || ld_w % 32 == 0), ZQ_ERR_USAGE,
+               "weight row stride %lld must be >= K and a multiple of 16 (32 for int4)",
+               (long long)ld_w);
+  ZQ_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) & 15) == 0 && (reinterpret_cast<uintptr_t>(wq) & 15) == 0,
+               ZQ_ERR_USAGE, "operands must be 16-byte aligned");
+  // exactness guard (igemm.py:52-63): K * 127 * qmax_w < 2^31
+  const int64_t qmw = w_bits == 8 ? 127 : 7;
+  ZQ_CHECK_ARG(K * 127 * qmw < (1LL << 31), ZQ_ERR_USAGE,
+               "igemm overflow guard: inner dim %lld with 8x%d-bit operands can reach >= 2^31",
+               (long long)K, w_bits);
+  if (!get_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ZQ_ERR_CUDA;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const int bn = pick_bn(M, N);
+  CUtensorMap ta, tb;
+  int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  if (w_bits == 8) {
+    rc = make_tmap_u8(&tb, wq, N, K, ld_w, BLOCK_K, bn, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  } else {
+    // packed rows: ld_w/2 bytes (zero past K), box 64 B x bn rows, no swizzle
+    rc = make_tmap_u8(&tb, wq, N, ld_w / 2, ld_w / 2, BLOCK_K / 2, bn, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+    p.w4 = reinterpret_cast<const uint8_t*>(wq);
+    p.ld_w4 = ld_w / 2;
+  }
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  {
+    const int esz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : 4;
+    const bool scales_ok =
+        (p.row_scales == nullptr || (reinterpret_cast<uintptr_t>(p.row_scales) & 15) == 0) &&
+        (p.bias == nullptr || (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0);
+    p.tma_out = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0) && ((p.ld_out * esz) % 16 == 0) &&
+                scales_ok;
+    if (p.tma_out) {
+      cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+      cuuint64_t strides[1] = {(cuuint64_t)(p.ld_out * esz)};
+      cuuint32_t box[2] = {32, 32};
+      cuuint32_t estr[2] = {1, 1};
+      CUtensorMapDataType dt = kind == OUT_S32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                               : kind == OUT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                               : kind == OUT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+      CUresult r = g_encode(&tc, dt, 2, p.out, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) p.tma_out = 0;
+    }
+  }
+  p.num_n_tiles = (int)((N + bn - 1) / bn);
+  p.num_tiles = (int)((M + BLOCK_M - 1) / BLOCK_M) * p.num_n_tiles;
+  p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+  const bool w4 = w_bits == 4;
+  switch (kind) {
+    case OUT_S32: return w4 ? launch_gemm_bn<OUT_S32, 1>(bn, ta, tb, tc, p, st) : launch_gemm_bn<OUT_S32, 0>(bn, ta, tb, tc, p, st);
+    case OUT_F32: return w4 ? launch_gemm_bn<OUT_F32, 1>(bn, ta, tb, tc, p, st) : launch_gemm_bn<OUT_F32, 0>(bn, ta, tb, tc, p, st);
+    case OUT_F16: return w4 ? launch_gemm_bn<OUT_F16, 1>(bn, ta, tb, tc, p, st) : launch_gemm_bn<OUT_F16, 0>(bn, ta, tb, tc, p, st);
+    default: return w4 ? launch_gemm_bn<OUT_BF16, 1>(bn, ta, tb, tc, p, st) : launch_gemm_bn<OUT_BF16, 0>(bn, ta, tb, tc, p, st);
+  }
+}
+
+}  // namespace zq
+
+using namespace zq;
+
+extern "C" {
+
+const char* zq_version(void) { return "zq_b200 0.1.0 sm_100a tcgen05-i8"; }
+
+int zq_igemm_s32(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
+                 int64_t M, int64_t N, int64_t K, int32_t* acc, int64_t ld_acc, void* stream) {
+  ZQ_CHECK_ARG(ld_acc >= N, ZQ_ERR_USAGE, "accumulator row stride too small");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.out = acc;
+  p.ld_out = ld_acc;
+  return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, OUT_S32, p,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float static_scale,
+              const void* wq, int64_t ld_w, int w_bits, const float* w_row_scales,
+              const float* bias, int64_t M, int64_t N, int64_t K, void* out, int64_t ld_out,
+              int out_type, void* stream) {
+  ZQ_CHECK_ARG(out_type >= ZQ_OUT_F32 && out_type <= ZQ_OUT_BF16, ZQ_ERR_USAGE, "bad output type %d", out_type);
+  ZQ_CHECK_ARG(w_row_scales != nullptr, ZQ_ERR_USAGE, "weight row scales required");
+  ZQ_CHECK_ARG(ld_out >= N, ZQ_ERR_USAGE, "output row stride too small");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.out = out;
+  p.ld_out = ld_out;
+  p.token_scales = token_scales;
+  p.static_scale = static_scale;
+  p.row_scales = w_row_scales;
+  p.bias = bias;
+  const int kind = out_type == ZQ_OUT_F32 ? OUT_F32 : out_type == ZQ_OUT_F16 ? OUT_F16 : OUT_BF16;
+  return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, kind, p,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zq_dequant_epilogue(const int32_t* acc, int64_t ld_acc, const float* token_scales,
+                        float static_scale, const float* w_row_scales, const float* bias,
+                        int64_t M, int64_t N, void* out, int64_t ld_out, int out_type,
+                        void* stream) {
+  ZQ_CHECK_ARG(out_type >= ZQ_OUT_F32 && out_type <= ZQ_OUT_BF16, ZQ_ERR_USAGE, "bad output type %d", out_type);
+  ZQ_CHECK_ARG(M >= 1 && N >= 1 && ld_acc >= N && ld_out >= N, ZQ_ERR_SHAPE, "bad epilogue shape");
+  int64_t total = M * N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  epilogue_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      acc, ld_acc, token_scales, static_scale, w_row_scales, bias, M, N, out, ld_out, out_type);
+  ZQ_LAUNCH_CHECK("epilogue launch");
+  return ZQ_OK;
+}
+
+int zq_linear_full(const float* x, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
+                   const float* w_row_scales, const float* bias, int64_t M, int64_t N,
+                   int64_t K, float* out, int64_t ld_out, void* stream) {
+  ZQ_CHECK_ARG(w_bits == 8 || w_bits == 4, ZQ_ERR_USAGE, "unsupported weight bit width %d", w_bits);
+  ZQ_CHECK_ARG(M >= 1 && N >= 1 && K >= 1 && ld_x >= K && ld_w >= K && ld_out >= N, ZQ_ERR_SHAPE,
+               "bad full-precision linear shape");
+  dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+  full_linear_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      x, ld_x, w_bits == 8 ? reinterpret_cast<const int8_t*>(wq) : nullptr,
+      w_bits == 4 ? reinterpret_cast<const uint8_t*>(wq) : nullptr, ld_w, w_row_scales, bias, M, N,
+      K, out, ld_out);
+  ZQ_LAUNCH_CHECK("full linear launch");
+  return ZQ_OK;
+}
+
+}  // extern "C"

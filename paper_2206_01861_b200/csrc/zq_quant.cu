@@ -1,0 +1,697 @@
+// Bandwidth-bound quantization kernels:
+//   K1 token-wise activation quantize      quant.py:258-269
+//   K2 static activation quantize          quant.py:272-281 / :103-113
+//   K3 group-wise weight quantize (+INT4)  quant.py:236-255
+//   K4 (residual +) LayerNorm + quantize   igemm.py:150-157, tensor.py:59-73
+//   K5 GeLU + quantize                     igemm.py:160-161, tensor.py:76-83
+// All arithmetic that decides an int8 value or a scale is written with explicit
+// round-to-nearest intrinsics (no FMA contraction) so the results are
+// bit-identical to the reference's numpy arithmetic.
+#include <cuda_fp16.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "zq_common.cuh"
+
+namespace zq {
+
+static thread_local char g_err[512];
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// Row producers: what value each activation element holds before quantization.
+// ---------------------------------------------------------------------------
+struct IdentityOp {
+  __device__ __forceinline__ float operator()(float x) const { return x; }
+};
+
+// scipy.special.erf (scipy 1.18, the reference's erf: tensor.py:15, :83) is the
+// Cephes ndtr.c algorithm: odd symmetry, a (4,5) rational in x^2 on |x| <= 1,
+// and 1 - erfc(x) above, with erfc = exp(-x^2) * P8(x)/Q8(x) (x < 8) or
+// exp(-x^2) * R5(x)/S6(x).  Restated here op for op (round-to-nearest, no
+// contraction) so the f64 result matches scipy bit for bit; this matters for
+// x << 0, where 1 + erf(x) cancels and the last bits of erf survive into the
+// float32 GeLU.  Verified identical to scipy on 5.5e5 points (tools/erf_check.py).
+__device__ __forceinline__ double polevl_d(double x, const double* c, int n) {
+  double a = c[0];
+  for (int i = 1; i <= n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
+  return a;
+}
+__device__ __forceinline__ double p1evl_d(double x, const double* c, int n) {
+  double a = __dadd_rn(x, c[0]);
+  for (int i = 1; i < n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
+  return a;
+}
+__device__ __forceinline__ double cephes_erf(double x) {
+  const double T[5] = {9.60497373987051638749E0, 9.00260197203842689217E1,
+                       2.23200534594684319226E3, 7.00332514112805075473E3,
+                       5.55923013010394962768E4};
+  const double U[5] = {3.35617141647503099647E1, 5.21357949780152679795E2,
+                       4.59432382970980127987E3, 2.26290000613890934246E4,
+                       4.92673942608635921086E4};
+  const double P[9] = {2.46196981473530512524E-10, 5.64189564831068821977E-1,
+                       7.46321056442269912687E0,   4.86371970985681366614E1,
+                       1.96520832956077098242E2,   5.26445194995477358631E2,
+                       9.34528527171957607540E2,   1.02755188689515710272E3,
+                       5.57535335369399327526E2};
+  const double Q[8] = {1.32281951154744992508E1, 8.67072140885989742329E1,
+                       3.54937778887819891062E2, 9.75708501743205489753E2,
+                       1.82390916687909736289E3, 2.24633760818710981792E3,
+                       1.65666309194161350182E3, 5.57535340817727675546E2};
+  const double R[6] = {5.64189583547755073984E-1, 1.27536670759978104416E0,
+                       5.01905042251180477414E0,  6.16021097993053585195E0,
+                       7.40974269950448939160E0,  2.97886665372100240670E0};
+  const double S[6] = {2.26052863220117276590E0, 9.39603524938001434673E0,
+                       1.20489539808096656605E1, 1.70814450747565897222E1,
+                       9.60896809063285878198E0, 3.36907645100081516050E0};
+  const double kMaxLog = 7.09782712893383996843E2;
+  const bool neg = x < 0.0;
+  const double a = fabs(x);
+  double r;
+  if (a <= 1.0) {
+    const double z = __dmul_rn(a, a);
+    r = __ddiv_rn(__dmul_rn(a, polevl_d(z, T, 4)), p1evl_d(z, U, 5));
+  } else {
+    // erfc(a) for a > 1
+    const double z = -__dmul_rn(a, a);
+    double ec;
+    if (z < -kMaxLog) {
+      ec = 0.0;
+    } else {
+      const double e = exp(z);
+      double p, q;
+      if (a < 8.0) {
+        p = polevl_d(a, P, 8);
+        q = p1evl_d(a, Q, 8);
+      } else {
+        p = polevl_d(a, R, 5);
+        q = p1evl_d(a, S, 6);
+      }
+      ec = __ddiv_rn(__dmul_rn(e, p), q);
+    }
+    r = __dsub_rn(1.0, ec);
+  }
+  return neg ? -r : r;
+}
+
+// tensor.py:76-83: f32( (x64 * 0.5) * (1.0 + erf(x64 * (1/sqrt 2))) ), every op
+// in f64 round-to-nearest (no contraction), one final rounding to f32.
+struct GeluOp {
+  __device__ __forceinline__ float operator()(float x) const {
+    const double kInvSqrt2 = 0x1.6a09e667f3bccp-1;  // 1.0 / math.sqrt(2.0) in Python
+    double x64 = (double)x;
+    double e = cephes_erf(__dmul_rn(x64, kInvSqrt2));
+    return __double2float_rn(__dmul_rn(__dmul_rn(x64, 0.5), __dadd_rn(1.0, e)));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K1/K5: one CTA per row, row held in registers as float4 chunks.
+// Thread t owns chunks t, t+B, ..., t+(NC-1)B.
+// ---------------------------------------------------------------------------
+template <int NC, class Op>
+__global__ void __launch_bounds__(1024) rowquant_vec_kernel(
+    const float* __restrict__ x, int64_t cols, int64_t ld_x, int qm, Op op,
+    float* __restrict__ y_out, int8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales,
+    int32_t* __restrict__ flag) {
+  __shared__ uint32_t red[32];
+  const int64_t row = blockIdx.x;
+  const int cols4 = (int)(cols >> 2);
+  const float4* xr = reinterpret_cast<const float4*>(x + row * ld_x);
+  float4 v[NC];
+  float amax = 0.0f;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    int c = threadIdx.x + i * blockDim.x;
+    if (c < cols4) {
+      float4 a = __ldg(xr + c);
+      a.x = op(a.x);
+      a.y = op(a.y);
+      a.z = op(a.z);
+      a.w = op(a.w);
+      bad |= !(is_finite_f(a.x) && is_finite_f(a.y) && is_finite_f(a.z) && is_finite_f(a.w));
+      amax = fmaxf(amax, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+      v[i] = a;
+    }
+  }
+  if (bad && flag) atomicOr(flag, 1);
+  amax = block_max_nonneg(amax, red);
+  const float s = scale_from_absmax(amax, qm);
+  if (threadIdx.x == 0) scales[row] = s;
+  char4* qr = reinterpret_cast<char4*>(q + row * ld_q);
+  float4* yr = y_out ? reinterpret_cast<float4*>(y_out + row * cols) : nullptr;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    int c = threadIdx.x + i * blockDim.x;
+    if (c < cols4) {
+      char4 o;
+      o.x = (signed char)quantize_exact(v[i].x, s, qm);
+      o.y = (signed char)quantize_exact(v[i].y, s, qm);
+      o.z = (signed char)quantize_exact(v[i].z, s, qm);
+      o.w = (signed char)quantize_exact(v[i].w, s, qm);
+      qr[c] = o;
+      if (yr) yr[c] = v[i];
+    }
+  }
+  // zero the K padding [cols, ld_q) so tensor-core K tails contribute nothing
+  const int ldq4 = (int)(ld_q >> 2);
+  for (int c = cols4 + threadIdx.x; c < ldq4; c += blockDim.x) qr[c] = make_char4(0, 0, 0, 0);
+}
+
+// Generic (any cols / alignment): two passes over the row, scalar loads.
+template <class Op>
+__global__ void __launch_bounds__(256) rowquant_scalar_kernel(
+    const float* __restrict__ x, int64_t cols, int64_t ld_x, int qm, Op op,
+    float* __restrict__ y_out, int8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales,
+    int32_t* __restrict__ flag) {
+  __shared__ uint32_t red[32];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * ld_x;
+  float amax = 0.0f;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float a = op(xr[c]);
+    bad |= !is_finite_f(a);
+    amax = fmaxf(amax, fabsf(a));
+  }
+  if (bad && flag) atomicOr(flag, 1);
+  amax = block_max_nonneg(amax, red);
+  const float s = scale_from_absmax(amax, qm);
+  if (threadIdx.x == 0) scales[row] = s;
+  int8_t* qr = q + row * ld_q;
+  for (int64_t c = threadIdx.x; c < ld_q; c += blockDim.x) {
+    if (c < cols) {
+      float a = op(xr[c]);
+      qr[c] = (int8_t)quantize_exact(a, s, qm);
+      if (y_out) y_out[row * cols + c] = a;
+    } else {
+      qr[c] = 0;
+    }
+  }
+}
+
+template <class Op>
+static int launch_rowquant(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int bits,
+                           Op op, float* y_out, int8_t* q, int64_t ld_q, float* scales,
+                           int32_t* flag, cudaStream_t st) {
+  const int qm = qmax_of(bits);
+  const bool vec = (cols % 4 == 0) && (ld_x % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_q % 16 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(q) & 15) == 0) &&
+                   (!y_out || (reinterpret_cast<uintptr_t>(y_out) & 15) == 0);
+  const int64_t cols4 = cols / 4;
+  if (vec && cols4 <= 1024 * 16) {
+    int nc = 1;
+    while ((cols4 + nc - 1) / nc > 1024 || ((cols4 + nc - 1) / nc > 256 && nc < 4)) nc *= 2;
+    int threads = (int)(((cols4 + nc - 1) / nc + 31) / 32 * 32);
+    if (threads < 32) threads = 32;
+    dim3 grid((unsigned)rows);
+    switch (nc) {
+      case 1: rowquant_vec_kernel<1, Op><<<grid, threads, 0, st>>>(x, cols, ld_x, qm, op, y_out, q, ld_q, scales, flag); break;
+      case 2: rowquant_vec_kernel<2, Op><<<grid, threads, 0, st>>>(x, cols, ld_x, qm, op, y_out, q, ld_q, scales, flag); break;
+      case 4: rowquant_vec_kernel<4, Op><<<grid, threads, 0, st>>>(x, cols, ld_x, qm, op, y_out, q, ld_q, scales, flag); break;
+      case 8: rowquant_vec_kernel<8, Op><<<grid, threads, 0, st>>>(x, cols, ld_x, qm, op, y_out, q, ld_q, scales, flag); break;
+      default: rowquant_vec_kernel<16, Op><<<grid, threads, 0, st>>>(x, cols, ld_x, qm, op, y_out, q, ld_q, scales, flag); break;
+    }
+  } else {
+    rowquant_scalar_kernel<Op><<<(unsigned)rows, 256, 0, st>>>(x, cols, ld_x, qm, op, y_out, q,
+                                                                ld_q, scales, flag);
+  }
+  ZQ_LAUNCH_CHECK("row quantize launch");
+  return ZQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2: static quantization, one scale for the whole tensor
+// ---------------------------------------------------------------------------
+__global__ void static_quant_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                    int64_t ld_x, float s32, double s64, int use_f32, int qm,
+                                    int8_t* __restrict__ q, int64_t ld_q,
+                                    int32_t* __restrict__ flag) {
+  const int64_t total = rows * ld_q;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / ld_q, c = i - r * ld_q;
+    int8_t o = 0;
+    if (c < cols) {
+      float a = x[r * ld_x + c];
+      bad |= !is_finite_f(a);
+      o = (int8_t)(use_f32 ? quantize_exact(a, s32, qm) : quantize_f64(a, s64, qm));
+    }
+    q[i] = o;
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Row max |x| (K3 phase 1, TP token absmax)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) row_absmax_kernel(const float* __restrict__ x,
+                                                         int64_t cols, int64_t ld_x,
+                                                         float* __restrict__ amax,
+                                                         int32_t* __restrict__ flag) {
+  __shared__ uint32_t red[32];
+  const float* xr = x + (int64_t)blockIdx.x * ld_x;
+  float m = 0.0f;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float a = xr[c];
+    bad |= !is_finite_f(a);
+    m = fmaxf(m, fabsf(a));
+  }
+  if (bad && flag) atomicOr(flag, 1);
+  m = block_max_nonneg(m, red);
+  if (threadIdx.x == 0) amax[blockIdx.x] = m;
+}
+
+// K3 phase 2: group max -> scale (quant.py:249-252), expanded row scales.
+__global__ void group_scale_kernel(const float* __restrict__ row_amax, int64_t rows,
+                                   int64_t groups, int qm, float* __restrict__ group_scales,
+                                   float* __restrict__ row_scales) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  const int64_t base = rows / groups;
+  const int64_t start = g * base;
+  const int64_t count = (g == groups - 1) ? rows - start : base;
+  float m = 0.0f;
+  for (int64_t r = 0; r < count; ++r) m = fmaxf(m, row_amax[start + r]);
+  float s = scale_from_absmax(m, qm);
+  group_scales[g] = s;
+  for (int64_t r = 0; r < count; ++r) row_scales[start + r] = s;
+}
+
+// K3 phase 3: quantize every row with its group scale; optional INT4 pack.
+__global__ void rowscale_quant_kernel(const float* __restrict__ w, int64_t rows, int64_t cols,
+                                      const float* __restrict__ row_scales, int qm,
+                                      int8_t* __restrict__ q, int64_t ld_q) {
+  const int64_t total = rows * ld_q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / ld_q, c = i - r * ld_q;
+    q[i] = (c < cols) ? (int8_t)quantize_exact(w[r * cols + c], row_scales[r], qm) : (int8_t)0;
+  }
+}
+
+__global__ void pack_int4_kernel(const int8_t* __restrict__ q, int64_t rows, int64_t ld_q,
+                                 uint8_t* __restrict__ packed) {
+  const int64_t half = ld_q / 2;
+  const int64_t total = rows * half;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / half, k = i - r * half;
+    uint8_t lo = (uint8_t)q[r * ld_q + 2 * k] & 0xF;
+    uint8_t hi = (uint8_t)q[r * ld_q + 2 * k + 1] & 0xF;
+    packed[i] = (uint8_t)(lo | (hi << 4));
+  }
+}
+
+// TP: quantize with a given (all-reduced) per-row absmax.
+__global__ void quant_with_absmax_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                         int64_t ld_x, const float* __restrict__ amax, int qm,
+                                         int8_t* __restrict__ q, int64_t ld_q,
+                                         float* __restrict__ scales) {
+  const int64_t total = rows * ld_q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / ld_q, c = i - r * ld_q;
+    float s = scale_from_absmax(amax[r], qm);
+    if (c == 0) scales[r] = s;
+    q[i] = (c < cols) ? (int8_t)quantize_exact(x[r * ld_x + c], s, qm) : (int8_t)0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: (residual +) LayerNorm + token-wise quantize, numpy pairwise reductions.
+// ---------------------------------------------------------------------------
+// numpy's float32 pairwise sum (see oracle.lowbit_oracle.pairwise_sum_f32):
+// leaves of <=128 elements, each summed with 8 interleaved accumulators
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail; leaves
+// combined by the binary split tree n2 = (n/2) rounded down to a multiple of 8.
+// The plan (computed on the host per row width) lists the leaves and the
+// internal-node combines level by level, so the tree is evaluated in parallel.
+constexpr int kMaxLeaves = 256;
+constexpr int kMaxNodes = 2 * kMaxLeaves;
+constexpr int kMaxLevels = 24;
+
+struct PairwisePlan {
+  int n;
+  int nleaves;
+  int nlevels;
+  int root;
+  int leaf_start[kMaxLeaves];
+  short leaf_len[kMaxLeaves];
+  short level_begin[kMaxLevels + 1];
+  short op_dst[kMaxLeaves];
+  short op_a[kMaxLeaves];
+  short op_b[kMaxLeaves];
+};
+
+struct PlanBuilder {
+  PairwisePlan* p;
+  int next_slot;
+  int depth_of[kMaxNodes];
+  int ops_dst[kMaxLeaves], ops_a[kMaxLeaves], ops_b[kMaxLeaves], ops_h[kMaxLeaves];
+  int nops;
+  bool ok;
+  // returns (slot, height)
+  int rec(int start, int n, int* height) {
+    if (n <= 128) {
+      if (p->nleaves >= kMaxLeaves) {
+        ok = false;
+        *height = 0;
+        return 0;
+      }
+      int id = p->nleaves++;
+      p->leaf_start[id] = start;
+      p->leaf_len[id] = (short)n;
+      *height = 0;
+      return id;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    int ha, hb;
+    int a = rec(start, n2, &ha);
+    int b = rec(start + n2, n - n2, &hb);
+    int h = (ha > hb ? ha : hb) + 1;
+    if (nops >= kMaxLeaves) {
+      ok = false;
+      *height = h;
+      return 0;
+    }
+    ops_a[nops] = a;
+    ops_b[nops] = b;
+    ops_h[nops] = h;
+    ops_dst[nops] = -1;
+    *height = h;
+    return -(++nops);  // negative: internal node index
+  }
+};
+
+static bool build_plan(int n, PairwisePlan* plan) {
+  memset(plan, 0, sizeof(*plan));
+  plan->n = n;
+  PlanBuilder b;
+  b.p = plan;
+  b.nops = 0;
+  b.ok = true;
+  int h;
+  int root = b.rec(0, n, &h);
+  if (!b.ok || h > kMaxLevels) return false;
+  // slot numbering: leaves 0..L-1, internal node i (1-based) -> L + i - 1
+  auto slot = [&](int s) { return s >= 0 ? s : plan->nleaves + (-s) - 1; };
+  plan->root = slot(root);
+  plan->nlevels = h;
+  int k = 0;
+  for (int lev = 1; lev <= h; ++lev) {
+    plan->level_begin[lev - 1] = (short)k;
+    for (int i = 0; i < b.nops; ++i)
+      if (b.ops_h[i] == lev) {
+        plan->op_dst[k] = (short)(plan->nleaves + i);
+        plan->op_a[k] = (short)slot(b.ops_a[i]);
+        plan->op_b[k] = (short)slot(b.ops_b[i]);
+        ++k;
+      }
+  }
+  plan->level_begin[h] = (short)k;
+  return true;
+}
+
+// Pairwise sum of f(row[i]) over the plan.  All threads of the block call it.
+// `slots` has >= 2*nleaves floats.
+template <class F>
+__device__ float pairwise_sum_block(const float* row, const PairwisePlan& plan, F f,
+                                    float* slots) {
+  const int n = plan.n;
+  if (n < 8) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float r = 0.0f;
+      for (int i = 0; i < n; ++i) r = __fadd_rn(r, f(row[i]));
+      slots[0] = r;
+    }
+    __syncthreads();
+    return slots[0];
+  }
+  // chains: thread handles (leaf = c >> 3, j = c & 7); lanes of one leaf are an
+  // aligned group of 8 so the 8-accumulator combine is a 3-step butterfly.
+  const int nchains = plan.nleaves * 8;
+  for (int base = 0; base < nchains; base += blockDim.x) {
+    int c = base + threadIdx.x;
+    float acc = 0.0f;
+    int leaf = c >> 3, j = c & 7;
+    bool act = c < nchains;
+    int len = 0, st = 0;
+    if (act) {
+      len = plan.leaf_len[leaf];
+      st = plan.leaf_start[leaf];
+      int m = len - len % 8;
+      acc = f(row[st + j]);
+      for (int i = 8 + j; i < m; i += 8) acc = __fadd_rn(acc, f(row[st + i]));
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) : IEEE addition is commutative, so
+    // the butterfly reproduces the fixed tree exactly.
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    if (act && j == 0) {
+      int m = len - len % 8;
+      for (int i = m; i < len; ++i) acc = __fadd_rn(acc, f(row[st + i]));
+      slots[leaf] = acc;
+    }
+  }
+  __syncthreads();
+  for (int lev = 0; lev < plan.nlevels; ++lev) {
+    int b = plan.level_begin[lev], e = plan.level_begin[lev + 1];
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x)
+      slots[plan.op_dst[k]] = __fadd_rn(slots[plan.op_a[k]], slots[plan.op_b[k]]);
+    __syncthreads();
+  }
+  float r = slots[plan.root];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) ln_quant_kernel(
+    const float* __restrict__ x, const float* __restrict__ res, const float* __restrict__ gamma,
+    const float* __restrict__ beta, int64_t cols, float eps, int qm,
+    const __grid_constant__ PairwisePlan plan, float* __restrict__ ln_out,
+    int8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales,
+    int32_t* __restrict__ flag) {
+  extern __shared__ float sm[];
+  __shared__ uint32_t red[32];
+  float* row = sm;                 // cols floats
+  float* slots = sm + cols;        // 2 * nleaves floats
+  const int64_t r = blockIdx.x;
+  const float* xr = x + r * cols;
+  const float* rr = res ? res + r * cols : nullptr;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float v = xr[c];
+    if (rr) v = __fadd_rn(v, rr[c]);  // (x + attn_out) / (h + f), transformer.py:477,486
+    bad |= !is_finite_f(v);
+    row[c] = v;
+  }
+  if (bad && flag) atomicOr(flag, 1);
+  __syncthreads();
+  const float fcols = (float)cols;
+  const float sum = pairwise_sum_block(row, plan, [](float v) { return v; }, slots);
+  const float mean = __fdiv_rn(sum, fcols);
+  const float sq = pairwise_sum_block(
+      row, plan,
+      [mean](float v) {
+        float d = __fsub_rn(v, mean);
+        return __fmul_rn(d, d);
+      },
+      slots);
+  const float var = __fdiv_rn(sq, fcols);
+  const float den = __fsqrt_rn(__fadd_rn(var, eps));
+  float amax = 0.0f;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float nv = __fdiv_rn(__fsub_rn(row[c], mean), den);
+    float y = __fadd_rn(__fmul_rn(nv, gamma[c]), beta[c]);
+    row[c] = y;
+    amax = fmaxf(amax, fabsf(y));
+    bad |= !is_finite_f(y);
+  }
+  if (bad && flag) atomicOr(flag, 1);
+  amax = block_max_nonneg(amax, red);  // contains __syncthreads
+  const float s = scale_from_absmax(amax, qm);
+  if (threadIdx.x == 0) scales[r] = s;
+  int8_t* qr = q + r * ld_q;
+  for (int64_t c = threadIdx.x; c < ld_q; c += blockDim.x) {
+    if (c < cols) {
+      float y = row[c];
+      qr[c] = (int8_t)quantize_exact(y, s, qm);
+      if (ln_out) ln_out[r * cols + c] = y;
+    } else {
+      qr[c] = 0;
+    }
+  }
+}
+
+struct PlanCache {
+  int n = -1;
+  PairwisePlan plan;
+};
+static thread_local PlanCache g_plan_cache;
+
+}  // namespace zq
+
+using namespace zq;
+
+extern "C" {
+
+const char* zq_last_error(void) { return zq::g_err; }
+
+int zq_quantize_tokenwise(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int bits,
+                          int8_t* q, int64_t ld_q, float* token_scales, int32_t* flag,
+                          void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "activations must be (tokens x dim), got (%lld, %lld)",
+               (long long)rows, (long long)cols);
+  ZQ_CHECK_ARG(ld_x >= cols && ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimensions");
+  return launch_rowquant(x, rows, cols, ld_x, bits, IdentityOp{}, nullptr, q, ld_q, token_scales,
+                         flag, as_stream(stream));
+}
+
+int zq_gelu_quantize(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int bits,
+                     float* gelu_out, int8_t* q, int64_t ld_q, float* token_scales, int32_t* flag,
+                     void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "activations must be (tokens x dim)");
+  ZQ_CHECK_ARG(ld_x >= cols && ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimensions");
+  return launch_rowquant(x, rows, cols, ld_x, bits, GeluOp{}, gelu_out, q, ld_q, token_scales,
+                         flag, as_stream(stream));
+}
+
+int zq_quantize_static(const float* x, int64_t rows, int64_t cols, int64_t ld_x, double scale,
+                       int bits, int8_t* q, int64_t ld_q, int32_t* flag, void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(scale > 0.0, ZQ_ERR_USAGE, "calibrated scale must be > 0, got %g", scale);
+  ZQ_CHECK_ARG(rows >= 0 && cols >= 0 && ld_x >= cols && ld_q >= cols, ZQ_ERR_USAGE, "bad shape");
+  if (rows == 0) return ZQ_OK;
+  float s32 = (float)scale;
+  int use_f32 = ((double)s32 == scale) && s32 > 0.0f;
+  int64_t total = rows * ld_q;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  static_quant_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, rows, cols, ld_x, s32, scale,
+                                                             use_f32, qmax_of(bits), q, ld_q, flag);
+  ZQ_LAUNCH_CHECK("static quantize launch");
+  return ZQ_OK;
+}
+
+int zq_row_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x, float* amax,
+                  int32_t* flag, void* stream) {
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1 && ld_x >= cols, ZQ_ERR_USAGE, "bad shape");
+  row_absmax_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(x, cols, ld_x, amax, flag);
+  ZQ_LAUNCH_CHECK("row absmax launch");
+  return ZQ_OK;
+}
+
+int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x,
+                            const float* amax, int bits, int8_t* q, int64_t ld_q,
+                            float* token_scales, void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d", bits);
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1 && ld_x >= cols && ld_q >= cols && ld_q % 16 == 0,
+               ZQ_ERR_USAGE, "bad shape");
+  int64_t total = rows * ld_q;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  quant_with_absmax_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, rows, cols, ld_x, amax,
+                                                                  qmax_of(bits), q, ld_q,
+                                                                  token_scales);
+  ZQ_LAUNCH_CHECK("quantize with absmax launch");
+  return ZQ_OK;
+}
+
+int zq_quantize_weight_groupwise(const float* w, int64_t rows, int64_t cols, int64_t groups,
+                                 int bits, int8_t* q, int64_t ld_q, float* group_scales,
+                                 float* row_scales, uint8_t* packed4, int32_t* flag,
+                                 void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "weight matrix must be 2-d and non-empty");
+  ZQ_CHECK_ARG(groups >= 1 && groups <= rows, ZQ_ERR_USAGE, "group count %lld invalid for %lld rows",
+               (long long)groups, (long long)rows);
+  ZQ_CHECK_ARG(ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimension");
+  ZQ_CHECK_ARG(!packed4 || bits == 4, ZQ_ERR_USAGE, "int4 packing requires bits == 4");
+  cudaStream_t st = as_stream(stream);
+  // row maxima go to row_scales (overwritten by the expanded scales in phase 2)
+  float* row_amax = nullptr;
+  if (cudaMallocAsync(&row_amax, sizeof(float) * rows, st) != cudaSuccess) {
+    set_error("cudaMallocAsync failed");
+    return ZQ_ERR_CUDA;
+  }
+  row_absmax_kernel<<<(unsigned)rows, 256, 0, st>>>(w, cols, cols, row_amax, flag);
+  group_scale_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, st>>>(row_amax, rows, groups,
+                                                                       qmax_of(bits),
+                                                                       group_scales, row_scales);
+  int64_t total = rows * ld_q;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  rowscale_quant_kernel<<<blocks, 256, 0, st>>>(w, rows, cols, row_scales, qmax_of(bits), q, ld_q);
+  if (packed4) {
+    int64_t tp = rows * (ld_q / 2);
+    int pb = (int)((tp + 255) / 256);
+    if (pb > 148 * 32) pb = 148 * 32;
+    pack_int4_kernel<<<pb, 256, 0, st>>>(q, rows, ld_q, packed4);
+  }
+  cudaFreeAsync(row_amax, st);
+  ZQ_LAUNCH_CHECK("group-wise weight quantize launch");
+  return ZQ_OK;
+}
+
+int zq_pack_int4(const int8_t* q, int64_t rows, int64_t ld_q, uint8_t* packed, void* stream) {
+  ZQ_CHECK_ARG(rows >= 1 && ld_q >= 2 && ld_q % 2 == 0, ZQ_ERR_USAGE, "bad shape for int4 pack");
+  int64_t tp = rows * (ld_q / 2);
+  int pb = (int)((tp + 255) / 256);
+  if (pb > 148 * 32) pb = 148 * 32;
+  pack_int4_kernel<<<pb, 256, 0, as_stream(stream)>>>(q, rows, ld_q, packed);
+  ZQ_LAUNCH_CHECK("int4 pack launch");
+  return ZQ_OK;
+}
+
+int zq_layer_norm_quantize(const float* x, const float* residual, const float* gamma,
+                           const float* beta, int64_t rows, int64_t cols, float eps, int bits,
+                           float* ln_out, int8_t* q, int64_t ld_q, float* token_scales,
+                           int32_t* flag, void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "activations must be (tokens x dim)");
+  ZQ_CHECK_ARG(eps > 0.0f, ZQ_ERR_USAGE, "layer_norm eps must be > 0");
+  ZQ_CHECK_ARG(ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimension");
+  ZQ_CHECK_ARG(cols <= 32768, ZQ_ERR_UNSUPPORTED, "layer_norm_quantize supports rows up to 32768 wide");
+  if (g_plan_cache.n != (int)cols) {
+    if (!build_plan((int)cols, &g_plan_cache.plan)) {
+      g_plan_cache.n = -1;
+      set_error("pairwise plan overflow for width %lld", (long long)cols);
+      return ZQ_ERR_UNSUPPORTED;
+    }
+    g_plan_cache.n = (int)cols;
+  }
+  const PairwisePlan& plan = g_plan_cache.plan;
+  size_t smem = sizeof(float) * (cols + 2 * (size_t)plan.nleaves + 2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(ln_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  int threads = cols >= 2048 ? 256 : 128;
+  ln_quant_kernel<<<(unsigned)rows, threads, smem, as_stream(stream)>>>(
+      x, residual, gamma, beta, cols, eps, qmax_of(bits), plan, ln_out, q, ld_q, token_scales,
+      flag);
+  ZQ_LAUNCH_CHECK("layer_norm_quantize launch");
+  return ZQ_OK;
+}
+
+}  // extern "C"

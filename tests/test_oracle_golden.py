@@ -159,3 +159,15 @@ def test_error_taxonomy():
     O.check_overflow_guard(133000, 8, 8)
     with pytest.raises(O.UsageError):
         O.group_layout_for(4, 5)
+
+
+def test_cephes_erf_is_scipy_erf():
+    """Pins the f64 erf the GPU GeLU restates (csrc/zq_quant.cu cephes_erf)."""
+    from scipy.special import erf
+
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([rng.standard_normal(20000) * 3, rng.uniform(-8, 8, 20000),
+                         rng.uniform(-1, 1, 5000), rng.uniform(-30, 30, 2000), [0.0, 1.0, -1.0, 8.0]])
+    ref = erf(xs)
+    mine = np.asarray([O.cephes_erf(float(v)) for v in xs])
+    assert np.array_equal(mine, ref)

@@ -1,0 +1,238 @@
+"""GPU parity: quantizers (K1 token-wise, K2 static, K3 group-wise, K4 LN+quant,
+K5 GeLU+quant) vs the reference golden vectors and the numpy oracle.
+Bar: bit-exact int8 payloads and float32 scales."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lowbit_oracle as O
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+
+
+@pytest.fixture(scope="module")
+def zq():
+    from paper_2206_01861_b200 import igemm, quant
+
+    return quant, igemm
+
+
+def h(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def same_bits(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.dtype == np.float32:
+        return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.astype(np.float32).view(np.uint32))
+    return a.shape == b.shape and np.array_equal(a, b)
+
+
+def sha(*arrays):
+    hh = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        hh.update(str(a.dtype).encode())
+        hh.update(str(a.shape).encode())
+        hh.update(a.tobytes())
+    return hh.hexdigest()
+
+
+def test_tokenwise_golden(zq, golden, golden_meta):
+    quant, _ = zq
+    for name in golden_meta["cases"]["tok"] + ["tok_kat"]:
+        bits = 4 if name.endswith("_b4") else 8
+        qa = quant.quantize_activation_tokenwise(golden[name + "_x"], bits)
+        assert same_bits(h(qa.values), golden[name + "_q"]), name
+        assert same_bits(h(qa.token_scales), golden[name + "_s"]), name
+
+
+def test_tokenwise_padding_is_zero(zq):
+    quant, _ = zq
+    x = np.random.default_rng(0).standard_normal((5, 37)).astype(F32)
+    qa = quant.quantize_activation_tokenwise(x, 8)
+    store = qa.values.as_strided((5, qa.values.stride(0)), (qa.values.stride(0), 1))
+    assert not h(store)[:, 37:].any()
+
+
+def test_tokenwise_random_shapes_and_ties(zq):
+    quant, _ = zq
+    rng = np.random.default_rng(7)
+    for i in range(60):
+        t = int(rng.integers(1, 65))
+        d = int(rng.integers(1, 4097))
+        x = (rng.standard_normal((t, d)) * rng.uniform(0.01, 50)).astype(F32)
+        if i % 3 == 0:
+            x[0] = 0.0
+        if i % 4 == 1:  # plant exact ties k+0.5 at the row's own scale
+            s = np.asarray([O.compute_scale(r, 8) for r in x], np.float64)
+            k = rng.integers(0, 127, (t, d)) + 0.5
+            cand = (k * s[:, None]).astype(F32)
+            ok = (cand.astype(np.float64) == k * s[:, None]) & (np.abs(cand) < np.abs(x).max(1, keepdims=True))
+            x = np.where(ok & (rng.uniform(size=(t, d)) < 0.3), cand, x).astype(F32)
+        bits = 4 if i % 5 == 0 else 8
+        qa = quant.quantize_activation_tokenwise(x, bits)
+        q_ref, s_ref = O.quantize_activation_tokenwise(x, bits)
+        assert same_bits(h(qa.values), q_ref), (t, d, bits)
+        assert same_bits(h(qa.token_scales), s_ref), (t, d, bits)
+
+
+def test_tokenwise_c1_digest(zq, golden_meta):
+    quant, _ = zq
+    hh = golden_meta["hashes"]["c1"]
+    x = O.Rng(1).gaussian((4096, 768), std=1.0)
+    qa = quant.quantize_activation_tokenwise(x, 8)
+    assert sha(h(qa.values)) == hh["xq_values"]
+    assert sha(h(qa.token_scales)) == hh["xq_scales"]
+
+
+def test_tokenwise_errors(zq):
+    from paper_2206_01861_b200.errors import UsageError
+
+    quant, _ = zq
+    with pytest.raises(UsageError):
+        quant.quantize_activation_tokenwise(np.ones((2, 3), F32), 16)
+    with pytest.raises(ValueError):
+        quant.quantize_activation_tokenwise(np.array([[1.0, np.nan]], F32), 8)
+    with pytest.raises(ValueError):
+        quant.quantize_activation_tokenwise(np.array([[1.0], [np.inf]], F32), 8)
+    with pytest.raises(UsageError):
+        quant.quantize_activation_tokenwise(np.ones((3,), F32), 8)
+
+
+def test_static_golden(zq, golden, golden_meta):
+    quant, _ = zq
+    for name in golden_meta["cases"]["static"]:
+        bits = 4 if name.endswith("_b4") else 8
+        qa = quant.quantize_activation_static(golden[name + "_x"], float(golden[name + "_scale"][0]), bits)
+        assert same_bits(h(qa.values), golden[name + "_q"]), name
+
+
+def test_scalar_kats(zq):
+    from paper_2206_01861_b200.errors import UsageError
+
+    quant, _ = zq
+    assert quant.quantize_value(1.0, 2.0 / 127.0, 8) == 64  # test_quant.py:86-88
+    assert quant.quantize_value(-2.0, 2.0 / 127.0, 8) == -127
+    assert quant.quantize_value(0.0, 0.37, 4) == 0
+    assert quant.quantize_value(100.0, 0.01, 4) == 7 and quant.quantize_value(-100.0, 0.01, 4) == -7
+    assert quant.compute_scale(np.array([0.5, -2.0, 1.0], F32), 8) == float(F32(2.0 / 127.0))
+    assert quant.compute_scale(np.zeros(3, F32), 4) == 1.0
+    with pytest.raises(ValueError):
+        quant.quantize_value(float("inf"), 1.0, 8)
+    with pytest.raises(UsageError):
+        quant.quantize_value(1.0, 0.0, 8)
+    with pytest.raises(UsageError):
+        quant.compute_scale(np.array([], F32), 8)
+    with pytest.raises(ValueError):
+        quant.compute_scale(np.array([1.0, np.nan], F32), 8)
+
+
+def test_negation_symmetry_and_monotone(zq):
+    quant, _ = zq
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal(5000) * 10).astype(F32)
+    for bits in (4, 8):
+        s = quant.compute_scale(x, bits)
+        qp = h(quant.quantize_array(x, s, bits))
+        qn = h(quant.quantize_array(-x, s, bits))
+        assert np.array_equal(qn, -qp)
+        xs = np.sort(x)
+        q = h(quant.quantize_array(xs, 0.07, bits)).astype(np.int32)
+        assert np.all(np.diff(q) >= 0)
+
+
+def test_groupwise_golden(zq, golden, golden_meta):
+    quant, _ = zq
+    for name in golden_meta["cases"]["wq"]:
+        g = int(name.split("_g")[1].split("_")[0])
+        bits = 4 if name.endswith("_b4") else 8
+        qm = quant.quantize_weight_groupwise(golden[name + "_w"], g, bits)
+        assert same_bits(h(qm.values), golden[name + "_q"]), name
+        assert same_bits(h(qm.group_scales), golden[name + "_gs"]), name
+        assert same_bits(h(qm.row_scales()), golden[name + "_rs"]), name
+        assert qm.group_layout == [tuple(v) for v in golden[name + "_layout"].tolist()], name
+        if bits == 4:
+            packed = h(qm.packed4)[:, : (qm.cols + 1) // 2]
+            assert np.array_equal(O.unpack_int4(packed)[:, : qm.cols], golden[name + "_q"]), name
+
+
+def test_groupwise_errors_and_c1(zq, golden_meta):
+    from paper_2206_01861_b200.errors import UsageError
+
+    quant, _ = zq
+    with pytest.raises(UsageError):
+        quant.quantize_weight_groupwise(np.ones((4, 2), F32), 5, 8)
+    with pytest.raises(UsageError):
+        quant.quantize_weight_groupwise(np.ones((4, 2), F32), 0, 8)
+    with pytest.raises(ValueError):
+        quant.quantize_weight_groupwise(np.array([[1.0, np.inf]], F32), 1, 8)
+    hh = golden_meta["hashes"]["c1"]
+    w = O.Rng(0).gaussian((3072, 768), std=0.02)
+    qm = quant.quantize_weight_groupwise(w, 48, 8)
+    assert sha(h(qm.values)) == hh["wq_values"] and sha(h(qm.group_scales)) == hh["wq_scales"]
+
+
+def test_layer_norm_quantize_golden(zq, golden, golden_meta):
+    _, igemm = zq
+    for name in golden_meta["cases"]["fused"]:
+        x, g, b = golden[name + "_x"], golden[name + "_gamma"], golden[name + "_beta"]
+        ln = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        qa = igemm.layer_norm_quantize(x, g, b, 8, ln_out=ln)
+        assert same_bits(h(ln), golden[name + "_ln"]), name
+        assert same_bits(h(qa.values), golden[name + "_lnq"]), name
+        assert same_bits(h(qa.token_scales), golden[name + "_lns"]), name
+
+
+def test_layer_norm_residual_and_widths(zq):
+    _, igemm = zq
+    rng = np.random.default_rng(11)
+    for d in (1, 5, 8, 64, 96, 100, 129, 300, 768, 1000, 1024, 3072, 4096, 6144, 8192):
+        x = (rng.standard_normal((6, d)) * rng.uniform(0.2, 5)).astype(F32)
+        r = (rng.standard_normal((6, d)) * 0.5).astype(F32)
+        g = (1 + 0.1 * rng.standard_normal(d)).astype(F32)
+        b = (0.1 * rng.standard_normal(d)).astype(F32)
+        ln = torch.empty((6, d), dtype=torch.float32, device="cuda")
+        qa = igemm.layer_norm_quantize(x, g, b, 8, residual=r, ln_out=ln)
+        ref = O.layer_norm_numpy((x + r).astype(F32), g, b)
+        assert same_bits(h(ln), ref), d
+        q_ref, s_ref = O.quantize_activation_tokenwise(ref, 8)
+        assert same_bits(h(qa.values), q_ref) and same_bits(h(qa.token_scales), s_ref), d
+
+
+def test_ln_digest(zq, golden_meta):
+    _, igemm = zq
+    hh = golden_meta["hashes"]["ln_512x768"]
+    xl = O.Rng(2).gaussian((512, 768), std=1.0)
+    qa = igemm.layer_norm_quantize(xl, np.ones(768, F32), np.zeros(768, F32), 8)
+    assert sha(h(qa.values)) == hh["q"] and sha(h(qa.token_scales)) == hh["s"]
+
+
+def test_gelu_quantize_golden(zq, golden, golden_meta):
+    _, igemm = zq
+    for name in golden_meta["cases"]["fused"]:
+        x = golden[name + "_x"]
+        ge = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        qa = igemm.gelu_quantize(x, 8, gelu_out=ge)
+        assert same_bits(h(ge), golden[name + "_gelu"]), name
+        assert same_bits(h(qa.values), golden[name + "_geq"]), name
+        assert same_bits(h(qa.token_scales), golden[name + "_ges"]), name
+
+
+def test_gelu_digest_and_large(zq, golden_meta):
+    _, igemm = zq
+    hh = golden_meta["hashes"]["gelu_256x3072"]
+    xg = O.Rng(3).gaussian((256, 3072), std=1.0)
+    ge = torch.empty(xg.shape, dtype=torch.float32, device="cuda")
+    qa = igemm.gelu_quantize(xg, 8, gelu_out=ge)
+    assert sha(h(ge)) == hh["gelu"]
+    assert sha(h(qa.values)) == hh["q"] and sha(h(qa.token_scales)) == hh["s"]
+    # NeoX FFN width, decode-sized batch
+    x = (np.random.default_rng(5).standard_normal((16, 24576)) * 2).astype(F32)
+    qa = igemm.gelu_quantize(x, 8)
+    q_ref, s_ref = O.gelu_quantize(x, 8)
+    assert same_bits(h(qa.values), q_ref) and same_bits(h(qa.token_scales), s_ref)
