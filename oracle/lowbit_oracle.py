@@ -240,6 +240,16 @@ def matmul_f32(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.einsum("ip,pj->ij", a, b, optimize=False)
 
 
+# Integer GEMM used by quantized_linear: the exact f64-BLAS restatement by
+# default; `use_reference_cost_igemm(True)` switches to igemm.py:79's int64
+# matmul (single-threaded numpy) so CPU-baseline timings carry the reference's cost.
+_IGEMM = [igemm]
+
+
+def use_reference_cost_igemm(flag: bool) -> None:
+    _IGEMM[0] = igemm_int64 if flag else igemm
+
+
 def quantized_linear(x, wv, w_row_scales, bias, mode: str, static_scale=None, act_bits=8, w_bits=8):
     """pkg/src/lowbit/igemm.py:115-139.  mode in {"dynamic", "static", "full"}."""
     x = np.ascontiguousarray(x, dtype=F32)
@@ -250,11 +260,11 @@ def quantized_linear(x, wv, w_row_scales, bias, mode: str, static_scale=None, ac
     if mode == "dynamic":
         xv, s = quantize_activation_tokenwise(x, act_bits)
         check_overflow_guard(wv.shape[1], act_bits, w_bits)
-        return dequant_epilogue(igemm(xv, wv), s, w_row_scales, bias)
+        return dequant_epilogue(_IGEMM[0](xv, wv), s, w_row_scales, bias)
     if mode == "static":
         xv = quantize_activation_static(x, static_scale, act_bits)
         check_overflow_guard(wv.shape[1], act_bits, w_bits)
-        return dequant_epilogue(igemm(xv, wv), float(static_scale), w_row_scales, bias)
+        return dequant_epilogue(_IGEMM[0](xv, wv), float(static_scale), w_row_scales, bias)
     raise UsageError(mode)
 
 

@@ -1,0 +1,454 @@
+"""Caller of the hot path: ZeroQuant post-LN blocks on B200
+(mirror of pkg/src/lowbit/transformer.py:26-532).
+
+* `PrecisionConfig` / `default_group_count` / `hw_aligned` are host logic,
+  identical to the reference (transformer.py:43-143).
+* `quantize_block` quantizes the six weight GEMMs group-wise on device
+  (transformer.py:333-361) and additionally keeps q/k/v fused into one
+  [3d x d] matrix: the three reference GEMMs consume the same quantized x
+  (transformer.py:470-472), so one tcgen05 GEMM with concatenated output
+  channels is bit-identical to three.
+* `block_forward` keeps the reference's signature and per-site activation
+  dispatch (`_act_mode_for`, transformer.py:386-402); LayerNorm+quantize and
+  GeLU+quantize run fused, with the residual add folded into the LN kernel.
+* `EncoderEngine` is the batched, CUDA-graph-captured forward used for the
+  BERT-base / GPT benchmarks (batch x seq tokens per step).
+
+Attention (QK^T, softmax, PV) is float in the reference (transformer.py:413-440)
+and stays float here (fp32); it is outside the bit-exact contract, so block
+outputs are compared with a tolerance (tests/test_transformer_gpu.py).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import igemm, quant
+from .errors import ShapeError, UsageError
+from .igemm import DynamicAct, FullAct, StaticAct
+from .quant import QuantizedMatrix, as_device_f32
+
+GEMM_SITES = ("attn_in", "attn_proj_in", "ffc_in", "ffc_mid")
+WEIGHT_NAMES = ("w_q", "w_k", "w_v", "w_o", "w_h4h", "w_4hh")
+BIAS_NAMES = ("b_q", "b_k", "b_v", "b_o", "b_h4h", "b_4hh")
+MHSA_WEIGHTS = ("w_q", "w_k", "w_v", "w_o")
+FFC_WEIGHTS = ("w_h4h", "w_4hh")
+LN_EPS = 1e-5
+INIT_STD = 0.02
+
+
+class ActivationMode(Enum):
+    """transformer.py:36-40"""
+
+    FULL = "full"
+    INT8 = "int8"
+    INT8_ATTN_FULL = "int8_attn_full"
+
+
+@dataclass(frozen=True)
+class PrecisionConfig:
+    """transformer.py:43-126 (verbatim semantics)."""
+
+    mhsa_weight_bits: int | None
+    ffc_weight_bits: int | None
+    activation_mode: ActivationMode = ActivationMode.FULL
+    activation_static: bool = False
+    group_count: int = 16
+
+    def __post_init__(self):
+        for bits in (self.mhsa_weight_bits, self.ffc_weight_bits):
+            if bits is not None and bits not in quant.SUPPORTED_BITS:
+                raise UsageError(f"weight bits must be 4, 8 or full, got {bits}")
+        if (self.mhsa_weight_bits is None) != (self.ffc_weight_bits is None):
+            raise UsageError("mixed full/quantized sublayers are not supported: quantize both or neither")
+        if self.activation_static and self.activation_mode is ActivationMode.FULL:
+            raise UsageError("static activation quantization requires an A8-style mode")
+
+    @property
+    def quantizes_weights(self) -> bool:
+        return self.mhsa_weight_bits is not None
+
+    @classmethod
+    def full(cls) -> "PrecisionConfig":
+        return cls(mhsa_weight_bits=None, ffc_weight_bits=None)
+
+    @classmethod
+    def from_scheme(cls, scheme: str, group_count: int | None = None,
+                    activation_static: bool = False, hidden_dim: int | None = None) -> "PrecisionConfig":
+        label = scheme.strip().upper()
+        if not label.startswith("W") or "A" not in label:
+            raise UsageError(f"malformed scheme {scheme!r}; expected WxAy like W8A8 or W4/8A16")
+        w_part, a_part = label[1:].split("A", 1)
+        weight_map = {"16": (None, None), "8": (8, 8), "4/8": (8, 4)}
+        act_map = {"16": ActivationMode.FULL, "8": ActivationMode.INT8, "8/16": ActivationMode.INT8_ATTN_FULL}
+        if w_part not in weight_map or a_part not in act_map:
+            raise UsageError(
+                f"malformed scheme {scheme!r}; valid schemes: "
+                "W16A16, W8A16, W8A8, W8A8/16, W4/8A16, W4/8A8, W4/8A8/16")
+        mhsa, ffc = weight_map[w_part]
+        mode = act_map[a_part]
+        if activation_static and mode is ActivationMode.FULL:
+            raise UsageError(f"scheme {scheme!r} has no activations to calibrate")
+        g = group_count if group_count is not None else default_group_count(hidden_dim or 0)
+        return cls(mhsa_weight_bits=mhsa, ffc_weight_bits=ffc, activation_mode=mode,
+                   activation_static=activation_static, group_count=g)
+
+    def label(self) -> str:
+        w = {(None, None): "16", (8, 8): "8", (8, 4): "4/8"}[(self.mhsa_weight_bits, self.ffc_weight_bits)]
+        a = {ActivationMode.FULL: "16", ActivationMode.INT8: "8", ActivationMode.INT8_ATTN_FULL: "8/16"}[
+            self.activation_mode]
+        return f"W{w}A{a}"
+
+
+def default_group_count(hidden_dim: int) -> int:
+    """transformer.py:129-137"""
+    if hidden_dim >= 2048:
+        return 128
+    if hidden_dim >= 1024:
+        return 64
+    if hidden_dim >= 512:
+        return 48
+    return 16
+
+
+def hw_aligned(rows: int, groups: int) -> bool:
+    """transformer.py:140-143"""
+    return all(count % 16 == 0 for _, count in quant.group_layout_for(rows, groups))
+
+
+# ---------------------------------------------------------------------------
+# quantized block on device
+# ---------------------------------------------------------------------------
+
+
+def concat_quantized(mats: list[QuantizedMatrix]) -> QuantizedMatrix:
+    """Stack output channels of separately quantized matrices (same bits/cols).
+    Each keeps its own groups; the result is what three separate GEMMs see."""
+    bits = {m.bits for m in mats}
+    cols = {m.cols for m in mats}
+    if len(bits) != 1 or len(cols) != 1:
+        raise UsageError("concatenated matrices must share bit width and column count")
+    ld = mats[0].ld
+    rows = sum(m.rows for m in mats)
+    store = torch.zeros((rows, ld), dtype=torch.int8, device=mats[0].values.device)
+    layout, gs, rs = [], [], []
+    off = 0
+    for m in mats:
+        store[off: off + m.rows, : m.cols].copy_(m.values)
+        layout += [(s + off, c) for s, c in m.group_layout]
+        gs.append(m.group_scales)
+        rs.append(m.row_scales())
+        off += m.rows
+    out = QuantizedMatrix(values=store[:, : mats[0].cols], bits=bits.pop(), group_scales=torch.cat(gs),
+                          group_layout=layout, row_scale_vec=torch.cat(rs).contiguous())
+    if out.bits == 4:
+        out.packed4 = quant.pack_int4(out.values)
+    return out
+
+
+@dataclass
+class DeviceBlock:
+    """QuantizedBlock (transformer.py:182-208) resident in HBM, plus the fused
+    QKV matrix.  Biases / LN parameters stay float32 (transformer.py:350-359)."""
+
+    w_q: QuantizedMatrix
+    w_k: QuantizedMatrix
+    w_v: QuantizedMatrix
+    w_o: QuantizedMatrix
+    w_h4h: QuantizedMatrix
+    w_4hh: QuantizedMatrix
+    b_q: torch.Tensor
+    b_k: torch.Tensor
+    b_v: torch.Tensor
+    b_o: torch.Tensor
+    b_h4h: torch.Tensor
+    b_4hh: torch.Tensor
+    ln1_gamma: torch.Tensor
+    ln1_beta: torch.Tensor
+    ln2_gamma: torch.Tensor
+    ln2_beta: torch.Tensor
+    num_heads: int
+    w_qkv: QuantizedMatrix | None = None
+    b_qkv: torch.Tensor | None = None
+
+    @property
+    def dim(self) -> int:
+        return self.w_q.rows
+
+    def __post_init__(self):
+        mhsa_bits = {getattr(self, n).bits for n in MHSA_WEIGHTS}
+        ffc_bits = {getattr(self, n).bits for n in FFC_WEIGHTS}
+        if len(mhsa_bits) != 1 or len(ffc_bits) != 1:
+            raise UsageError("MHSA matrices must share one bit width, FFC another")
+        if self.dim % self.num_heads != 0:
+            raise UsageError(f"hidden dim {self.dim} not divisible by {self.num_heads} heads")
+        if self.w_qkv is None:
+            self.w_qkv = concat_quantized([self.w_q, self.w_k, self.w_v])
+            self.b_qkv = torch.cat([self.b_q, self.b_k, self.b_v]).contiguous()
+
+
+def _get(block, name):
+    return block[name] if isinstance(block, dict) else getattr(block, name)
+
+
+def quantize_block(block, precision: PrecisionConfig) -> DeviceBlock:
+    """transformer.py:333-361: group-wise quantization of the six weight GEMMs
+    with groups = min(g, rows); `block` is a BlockWeights-like object or dict of
+    float32 arrays (numpy or torch)."""
+    if not precision.quantizes_weights:
+        raise UsageError("the B200 path runs quantized blocks; use a W8/W4 scheme")
+    g = precision.group_count
+
+    def qm(name, bits):
+        w = as_device_f32(_get(block, name))
+        return quant.quantize_weight_groupwise(w, min(g, w.shape[0]), bits)
+
+    mb, fb = precision.mhsa_weight_bits, precision.ffc_weight_bits
+    vec = lambda n: as_device_f32(_get(block, n)).reshape(-1).contiguous()  # noqa: E731
+    return DeviceBlock(
+        w_q=qm("w_q", mb), w_k=qm("w_k", mb), w_v=qm("w_v", mb), w_o=qm("w_o", mb),
+        w_h4h=qm("w_h4h", fb), w_4hh=qm("w_4hh", fb),
+        b_q=vec("b_q"), b_k=vec("b_k"), b_v=vec("b_v"), b_o=vec("b_o"), b_h4h=vec("b_h4h"),
+        b_4hh=vec("b_4hh"), ln1_gamma=vec("ln1_gamma"), ln1_beta=vec("ln1_beta"),
+        ln2_gamma=vec("ln2_gamma"), ln2_beta=vec("ln2_beta"), num_heads=int(_get(block, "num_heads")),
+    )
+
+
+def random_block(dim: int, num_heads: int, mhsa_bits: int, ffc_bits: int, groups: int,
+                 seed: int = 0, ffn_mult: int = 4) -> DeviceBlock:
+    """Random-init block generated and quantized on device (Gaussian(0, 0.02)
+    weights, zero biases, identity LN — transformer.py:261-297's recipe, with a
+    device RNG so GPT-scale layers don't need a host round trip)."""
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+
+    def w(r, c):
+        return torch.randn((r, c), generator=gen, device="cuda") * INIT_STD
+
+    def qm(r, c, bits):
+        return quant.quantize_weight_groupwise(w(r, c), min(groups, r), bits)
+
+    z = lambda n: torch.zeros(n, device="cuda")  # noqa: E731
+    o = lambda n: torch.ones(n, device="cuda")  # noqa: E731
+    f = ffn_mult * dim
+    return DeviceBlock(
+        w_q=qm(dim, dim, mhsa_bits), w_k=qm(dim, dim, mhsa_bits), w_v=qm(dim, dim, mhsa_bits),
+        w_o=qm(dim, dim, mhsa_bits), w_h4h=qm(f, dim, ffc_bits), w_4hh=qm(dim, f, ffc_bits),
+        b_q=z(dim), b_k=z(dim), b_v=z(dim), b_o=z(dim), b_h4h=z(f), b_4hh=z(dim),
+        ln1_gamma=o(dim), ln1_beta=z(dim), ln2_gamma=o(dim), ln2_beta=z(dim), num_heads=num_heads)
+
+
+# ---------------------------------------------------------------------------
+# forward
+# ---------------------------------------------------------------------------
+
+
+def _act_mode_for(precision: PrecisionConfig, site: str, layer: int, static_scales):
+    """transformer.py:386-402"""
+    mode = precision.activation_mode
+    if mode is ActivationMode.FULL:
+        return FullAct()
+    if mode is ActivationMode.INT8_ATTN_FULL and site == "attn_in":
+        return FullAct()
+    if precision.activation_static:
+        key = f"layer{layer}.{site}"
+        if static_scales is None or key not in static_scales:
+            raise UsageError(f"static activation quantization needs a calibrated scale for {key}")
+        return StaticAct(scale=static_scales[key], bits=8)
+    return DynamicAct(bits=8)
+
+
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int, causal: bool,
+              batch: int = 1) -> torch.Tensor:
+    """transformer.py:413-440 on device, float32, for `batch` sequences packed as
+    [batch*t, d] rows (each sequence attends only to itself)."""
+    bt, d = q.shape
+    t = bt // batch
+    dh = d // num_heads
+
+    def heads(z):
+        return z.reshape(batch, t, num_heads, dh).transpose(1, 2)
+
+    ctx = torch.nn.functional.scaled_dot_product_attention(
+        heads(q), heads(k), heads(v), is_causal=causal, scale=float(np.float32(1.0 / math.sqrt(dh))))
+    return ctx.transpose(1, 2).reshape(bt, d).contiguous()
+
+
+def _linear_site(x, w: QuantizedMatrix, bias, am):
+    if isinstance(am, FullAct):
+        return igemm.full_linear(x, w, bias)
+    return igemm.quantized_linear(x, w, bias, am)
+
+
+def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: bool, layer: int = 0,
+                  static_scales: dict[str, float] | None = None, batch: int = 1) -> torch.Tensor:
+    """transformer.py:443-486: LN2(h + FFC(h)) with h = LN1(x + MHSA(x)).
+    Dynamic-activation sites run the fused kernels (LN/GeLU + quantize); the
+    result equals the reference up to attention's float rounding."""
+    xt = as_device_f32(x)
+    if xt.dim() != 2 or xt.shape[1] != block.dim:
+        raise ShapeError(f"block input {tuple(xt.shape)} does not match hidden dim {block.dim}")
+    t, d = xt.shape
+
+    def mode(site):
+        return _act_mode_for(precision, site, layer, static_scales)
+
+    am = mode("attn_in")
+    qkv = _linear_site(xt, block.w_qkv, block.b_qkv, am)
+    ctx = attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], block.num_heads, causal, batch)
+    attn_out = _linear_site(ctx, block.w_o, block.b_o, mode("attn_proj_in"))
+    h = torch.empty_like(xt)
+    m_ffc_in = mode("ffc_in")
+    if isinstance(m_ffc_in, DynamicAct):
+        hq = igemm.layer_norm_quantize(xt, block.ln1_gamma, block.ln1_beta, 8, LN_EPS, residual=attn_out, ln_out=h)
+        u = igemm.fused_linear(hq, block.w_h4h, block.b_h4h)
+    else:
+        igemm.layer_norm_quantize(xt, block.ln1_gamma, block.ln1_beta, 8, LN_EPS, residual=attn_out, ln_out=h)
+        u = _linear_site(h, block.w_h4h, block.b_h4h, m_ffc_in)
+    m_mid = mode("ffc_mid")
+    if isinstance(m_mid, DynamicAct):
+        zq = igemm.gelu_quantize(u, 8)
+        f = igemm.fused_linear(zq, block.w_4hh, block.b_4hh)
+    else:
+        z = torch.empty_like(u)
+        igemm.gelu_quantize(u, 8, gelu_out=z)
+        f = _linear_site(z, block.w_4hh, block.b_4hh, m_mid)
+    y = torch.empty_like(xt)
+    igemm.layer_norm_quantize(h, block.ln2_gamma, block.ln2_beta, 8, LN_EPS, residual=f, ln_out=y)
+    return y
+
+
+# ---------------------------------------------------------------------------
+# Batched encoder / decoder-prefill engine (the benchmark caller)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class EncoderEngine:
+    """Embedding -> L ZeroQuant blocks (W8A8 / W4/8A8, dynamic token-wise
+    activations) -> final LN, for `batch` sequences of `seq` tokens.
+
+    All intermediates are preallocated; `forward()` is a fixed launch sequence
+    that is captured once into a CUDA graph.  Per block:
+      QKV GEMM -> attention -> ctx quantize -> O GEMM -> (x+attn) LN1+quant ->
+      h4h GEMM -> GeLU+quant -> 4hh GEMM -> (h+f) LN2+quant (next block's input).
+    """
+
+    blocks: list[DeviceBlock]
+    embedding: torch.Tensor        # [V, d] float32
+    final_gamma: torch.Tensor
+    final_beta: torch.Tensor
+    batch: int
+    seq: int
+    causal: bool = False
+    use_graph: bool = True
+    _bufs: dict = field(default_factory=dict, init=False)
+    _graph: object = field(default=None, init=False)
+
+    def __post_init__(self):
+        d = self.embedding.shape[1]
+        t = self.batch * self.seq
+        f = self.blocks[0].w_h4h.rows
+        dev = self.embedding.device
+        e = lambda *s: torch.empty(s, dtype=torch.float32, device=dev)  # noqa: E731
+        self._bufs = dict(
+            ids=torch.zeros(t, dtype=torch.int64, device=dev),
+            x=e(t, d), h=e(t, d), qkv=e(t, 3 * d), ctx=e(t, d), attn=e(t, d), u=e(t, f), f=e(t, d),
+            out=e(t, d),
+            xq=quant.padded_int8(t, d), cq=quant.padded_int8(t, d), hq=quant.padded_int8(t, d),
+            zq=quant.padded_int8(t, f), sx=e(t), sc=e(t), sh=e(t), sz=e(t),
+            flag=torch.zeros(1, dtype=torch.int32, device=dev),
+        )
+
+    @property
+    def tokens(self) -> int:
+        return self.batch * self.seq
+
+    # -- raw launches (no allocation, no host sync) --------------------------
+    def _linear(self, q, s, w: QuantizedMatrix, bias, out):
+        t, k = q.shape
+        wp, ldw, wb = w.weight_operand()
+        N.call("zq_linear", q.data_ptr(), q.stride(0), s.data_ptr(), 0.0, wp, ldw, wb,
+               w.row_scales().data_ptr(), bias.data_ptr(), t, w.rows, k, out.data_ptr(), out.stride(0),
+               N.OUT_F32, N.stream_ptr())
+
+    def _ln_quant(self, x, res, g, b, ln_out, q, s):
+        t, d = x.shape
+        N.call("zq_layer_norm_quantize", x.data_ptr(), N.ptr(res), g.data_ptr(), b.data_ptr(), t, d,
+               float(np.float32(LN_EPS)), 8, ln_out.data_ptr(), q.data_ptr(), q.stride(0), s.data_ptr(),
+               self._bufs["flag"].data_ptr(), N.stream_ptr())
+
+    def _tok_quant(self, x, q, s):
+        t, d = x.shape
+        N.call("zq_quantize_tokenwise", x.data_ptr(), t, d, d, 8, q.data_ptr(), q.stride(0), s.data_ptr(),
+               self._bufs["flag"].data_ptr(), N.stream_ptr())
+
+    def _gelu_quant(self, u, q, s):
+        t, f = u.shape
+        N.call("zq_gelu_quantize", u.data_ptr(), t, f, f, 8, None, q.data_ptr(), q.stride(0), s.data_ptr(),
+               self._bufs["flag"].data_ptr(), N.stream_ptr())
+
+    def _run(self):
+        B = self._bufs
+        d = self.embedding.shape[1]
+        torch.index_select(self.embedding, 0, B["ids"], out=B["x"])
+        self._tok_quant(B["x"], B["xq"], B["sx"])
+        x, xq, sx = B["x"], B["xq"], B["sx"]
+        for blk in self.blocks:
+            self._linear(xq, sx, blk.w_qkv, blk.b_qkv, B["qkv"])
+            qkv = B["qkv"]
+            B["ctx"].copy_(attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads,
+                                     self.causal, self.batch))
+            self._tok_quant(B["ctx"], B["cq"], B["sc"])
+            self._linear(B["cq"], B["sc"], blk.w_o, blk.b_o, B["attn"])
+            self._ln_quant(x, B["attn"], blk.ln1_gamma, blk.ln1_beta, B["h"], B["hq"], B["sh"])
+            self._linear(B["hq"], B["sh"], blk.w_h4h, blk.b_h4h, B["u"])
+            self._gelu_quant(B["u"], B["zq"], B["sz"])
+            self._linear(B["zq"], B["sz"], blk.w_4hh, blk.b_4hh, B["f"])
+            # y = LN2(h + f) is the next block's input; its quantization is fused
+            self._ln_quant(B["h"], B["f"], blk.ln2_gamma, blk.ln2_beta, x, xq, sx)
+        self._ln_quant(x, None, self.final_gamma, self.final_beta, B["out"], B["cq"], B["sc"])
+
+    def capture(self):
+        """Warm up and capture the whole forward into one CUDA graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self._run()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._run()
+        self._graph = g
+        return g
+
+    def launch(self):
+        """Enqueue one forward on the current stream (ids already in _bufs['ids'])."""
+        if self.use_graph:
+            if self._graph is None:
+                self.capture()
+            self._graph.replay()
+        else:
+            self._run()
+
+    def forward(self, token_ids) -> torch.Tensor:
+        """token ids [batch, seq] (host or device) -> final hidden [batch*seq, d]
+        on device.  Raises ValueError if any activation went non-finite."""
+        ids = token_ids if isinstance(token_ids, torch.Tensor) else torch.as_tensor(np.asarray(token_ids))
+        if tuple(ids.shape) != (self.batch, self.seq):
+            raise ShapeError(f"expected token ids of shape {(self.batch, self.seq)}, got {tuple(ids.shape)}")
+        self._bufs["ids"].copy_(ids.reshape(-1), non_blocking=True)
+        self._bufs["flag"].zero_()
+        self.launch()
+        return self._bufs["out"]
+
+    def check_finite(self):
+        if int(self._bufs["flag"].item()) != 0:
+            raise ValueError("non-finite activations encountered in the forward")

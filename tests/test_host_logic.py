@@ -1,0 +1,113 @@
+"""CPU: host-side logic of the product package (no GPU): scheme parsing,
+group defaults, layouts, error taxonomy, and that the C-ABI library exports
+every symbol include/zq_b200.h declares."""
+
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_scheme_parsing():
+    from paper_2206_01861_b200.transformer import ActivationMode, PrecisionConfig
+
+    cases = [("W16A16", None, None, ActivationMode.FULL), ("W8A16", 8, 8, ActivationMode.FULL),
+             ("W8A8", 8, 8, ActivationMode.INT8), ("W4/8A16", 8, 4, ActivationMode.FULL),
+             ("W4/8A8", 8, 4, ActivationMode.INT8), ("W8A8/16", 8, 8, ActivationMode.INT8_ATTN_FULL)]
+    for label, mhsa, ffc, mode in cases:  # test_transformer.py:60-76
+        p = PrecisionConfig.from_scheme(label)
+        assert (p.mhsa_weight_bits, p.ffc_weight_bits, p.activation_mode) == (mhsa, ffc, mode)
+        assert p.label() == label
+
+
+@pytest.mark.parametrize("bad", ["W2A8", "A8", "W8", "W8A3", "8A8", "W4A8"])
+def test_malformed_scheme(bad):
+    from paper_2206_01861_b200.errors import UsageError
+    from paper_2206_01861_b200.transformer import PrecisionConfig
+
+    with pytest.raises(UsageError):
+        PrecisionConfig.from_scheme(bad)
+
+
+def test_group_defaults_and_alignment():
+    from paper_2206_01861_b200.transformer import default_group_count, hw_aligned
+
+    assert [default_group_count(d) for d in (768, 512, 1024, 2048, 64)] == [48, 48, 64, 128, 16]
+    assert hw_aligned(768, 48) and not hw_aligned(64, 16) and hw_aligned(256, 16)
+
+
+def test_precision_validation():
+    from paper_2206_01861_b200.errors import UsageError
+    from paper_2206_01861_b200.transformer import ActivationMode, PrecisionConfig
+
+    with pytest.raises(UsageError):
+        PrecisionConfig(mhsa_weight_bits=8, ffc_weight_bits=None)
+    with pytest.raises(UsageError):
+        PrecisionConfig(8, 8, ActivationMode.FULL, activation_static=True)
+
+
+def test_group_layout_and_quantspec():
+    from paper_2206_01861_b200 import quant
+    from paper_2206_01861_b200.errors import UsageError
+
+    assert quant.group_layout_for(4, 2) == [(0, 2), (2, 2)]
+    assert quant.group_layout_for(5, 2) == [(0, 2), (2, 3)]
+    with pytest.raises(UsageError):
+        quant.group_layout_for(4, 5)
+    with pytest.raises(UsageError):
+        quant.QuantSpec(bits=8, granularity=quant.Granularity.PER_GROUP, for_weights=False)
+    with pytest.raises(UsageError):
+        quant.QuantSpec(bits=8, granularity=quant.Granularity.PER_TOKEN, for_weights=True)
+    with pytest.raises(UsageError):
+        quant.QuantSpec(bits=8, granularity=quant.Granularity.PER_TOKEN, mode=quant.Mode.STATIC,
+                        for_weights=False)
+    quant.QuantSpec(bits=8, granularity=quant.Granularity.PER_TENSOR, mode=quant.Mode.STATIC)
+    assert quant.qmax(8) == 127 and quant.qmax(4) == 7
+
+
+def test_overflow_guard_host():
+    from paper_2206_01861_b200 import igemm
+    from paper_2206_01861_b200.errors import UsageError
+
+    igemm.check_overflow_guard(133000, 8, 8)
+    with pytest.raises(UsageError):
+        igemm.check_overflow_guard(140000, 8, 8)
+
+
+def test_calibrator_host_rules():
+    from paper_2206_01861_b200 import quant
+    from paper_2206_01861_b200.errors import UsageError
+
+    with pytest.raises(UsageError):
+        quant.Calibrator(momentum=1.0)
+    with pytest.raises(UsageError):
+        quant.Calibrator().finalize(8)
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+
+    from paper_2206_01861_b200 import _native
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    _native._lib = None
+    with pytest.raises(_native.NativeUnavailable):
+        _native.load()
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2206_01861_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built (run __graft_entry__.build())")
+    with open(os.path.join(ROOT, "include", "zq_b200.h")) as f:
+        header = f.read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(zq_\w+)\s*\(", header, re.M))
+    assert declared, "no declarations parsed"
+    lib = _native.load_for_inspection()
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert declared == set(_native.exported_symbols())
