@@ -135,6 +135,12 @@ int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t 
                             const float* amax, int bits, int8_t* q, int64_t ld_q,
                             float* token_scales, void* stream);
 
+/* Diagnostics: when buf != NULL, subsequent GEMM launches record per-CTA
+ * %globaltimer stamps into buf[cta*64 + slot] (slot 0 entry, 1 setup done,
+ * 2+4t / 3+4t MMA start / last operands landed for local tile t, 4+4t / 5+4t
+ * epilogue start / end, 63 epilogue exit).  Not thread-safe; tooling only. */
+int zq_gemm_set_trace(unsigned long long* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,54 @@ __device__ __forceinline__ int quantize_exact(float x, float s, int qm) {
   return x < 0.0f ? -k : k;
 }
 
+// Out-of-line copy for rarely taken fallbacks (keeps hot loops small in I$).
+static __device__ __noinline__ int quantize_exact_slow(float x, float s, int qm) {
+  return quantize_exact(x, s, qm);
+}
+
+// Fast exact variant.  r = |x| * (1/s) with the correctly rounded reciprocal
+// is within 2^-15 (absolute, for r < 200) of the true quotient q.  RHAFZ(q) is
+// the integer nearest q (ties away), so rint(r) is exact unless q is within
+// that error of a half-integer; the magic-number rounding (r + 1.5*2^23 rounds
+// to an integer in the FMA pipe) gives rint(r) and the distance to it, and
+// near-ties (|d - 1/2| < 2^-14: ~1e-4 of elements, and every planted tie) take
+// the exact path above.  `inv` = safe_rcp(s); inv == 0 forces the exact path.
+__device__ __forceinline__ int quantize_fast(float x, float s, float inv, int qm) {
+  const float r = __fmul_rn(fabsf(x), inv);
+  int k;
+  if (r >= 200.0f) {
+    k = qm;
+  } else {
+    const float m = __fadd_rn(r, 12582912.0f);        // RN(r) in the low mantissa bits
+    const float d = fabsf(__fsub_rn(r, __fsub_rn(m, 12582912.0f)));  // |r - rint(r)|, exact
+    if (d > 0.49993896484375f || inv == 0.0f) return quantize_exact_slow(x, s, qm);
+    k = min(__float_as_int(m) - 0x4B400000, qm);
+  }
+  return x < 0.0f ? -k : k;
+}
+
+// |x| as a u32 bit pattern: monotone for finite values, and inf/NaN compare
+// above every finite value, so one max tracks both the row max and the
+// non-finite flag (bits >= 0x7f800000).
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+
+// Correctly rounded a / b given y = RN(1/b) (Markstein: q = RN(a*y) is within
+// 1 ulp, r = a - b*q is exact with an FMA, RN(q + r*y) = RN(a/b)), for
+// quotients and operands well inside the normal range; otherwise the IEEE
+// division.
+__device__ __forceinline__ float div_rn_fast(float a, float b, float y) {
+  const float q = __fmul_rn(a, y);
+  const float aq = fabsf(q);
+  if (!(aq > 1e-30f && aq < 1e30f) || !(fabsf(a) > 1e-30f)) return __fdiv_rn(a, b);
+  const float r = __fmaf_rn(-b, q, a);
+  return __fmaf_rn(r, y, q);
+}
+
+__device__ __forceinline__ float safe_rcp(float s) {
+  const float inv = __frcp_rn(s);
+  return (inv < 1e30f) ? inv : 0.0f;
+}
+
 // Static path with an arbitrary f64 scale: numpy's exact op sequence
 // (f64 divide, f64 add 0.5, floor, clip).
 __device__ __forceinline__ int quantize_f64(float x, double s, int qm) {
@@ -110,6 +158,12 @@ __device__ __forceinline__ float block_max_nonneg(float v, uint32_t* red) {
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_100a)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -43,6 +44,8 @@ struct GemmParams {
   const uint8_t* w4;          // packed int4 weights (W4 path), row stride ld_w4 bytes
   int64_t ld_w4;
   int tma_out;                // output tensor map valid -> staged TMA stores
+  unsigned long long* trace;  // diagnostics: per-CTA %globaltimer stamps (nullable)
+  int debug;                  // diagnostics: 1 = skip global stores, 2 = skip dequant math
 };
 
 template <int BN, int W4>
@@ -137,6 +140,29 @@ __device__ __forceinline__ void epi_chunk_smem(const uint32_t (&r)[32], float s_
   }
 }
 
+// Coalesced write-back of a staged 32x32 chunk: lane l handles 16-byte piece
+// (l % P) of row (l / P) + step * (32 / P), P = pieces per row (8 for 4-byte,
+// 4 for 2-byte outputs); rows past M are skipped.
+template <int KIND>
+__device__ __forceinline__ void store_chunk_coalesced(const uint8_t* stage, void* out, int64_t ld_out,
+                                                      int row0, int col0, int M, int lane) {
+  constexpr int ESZ = (KIND == OUT_F16 || KIND == OUT_BF16) ? 2 : 4;
+  constexpr int P = 32 * ESZ / 16;   // 16-byte pieces per row
+  constexpr int RPS = 32 / P;        // rows per store instruction
+  const int pc = lane % P, rr = lane / P;
+#pragma unroll
+  for (int st = 0; st < P; ++st) {
+    const int r = st * RPS + rr;
+    const int phys = (ESZ == 4) ? (pc ^ (r & 7)) : (pc ^ ((r >> 1) & 3));
+    const uint4 v = *reinterpret_cast<const uint4*>(stage + r * (32 * ESZ) + phys * 16);
+    if (row0 + r < M) {
+      uint8_t* dst = reinterpret_cast<uint8_t*>(out) +
+                     ((int64_t)(row0 + r) * ld_out + col0) * ESZ + pc * 16;
+      *reinterpret_cast<uint4*>(dst) = v;
+    }
+  }
+}
+
 // Ragged edge (N tail or unaligned output): element-wise, guarded.
 template <int KIND>
 __device__ __forceinline__ void epi_chunk_slow(const uint32_t (&r)[32], float s_tok,
@@ -184,6 +210,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * 64] = gtime();
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -206,6 +233,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int nkb = p.num_k_blocks;
+  unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
   if (warp == 0) {
     // ===================== TMA producer =====================
     // whole warp walks the loop (keeps the warp converged for the final
@@ -240,14 +269,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     constexpr uint32_t idesc = make_idesc_i8(BLOCK_M, BN);
-    int stage = 0, phase = 0, acc = 0, acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    int stage = 0, phase = 0, acc = 0, acc_phase = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
+      if (tr && lane == 0 && lt < 15) tr[2 + 4 * lt] = gtime();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
+        if (tr && lane == 0 && lt < 15 && kb == nkb - 1) tr[3 + 4 * lt] = gtime();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
@@ -281,8 +312,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
     uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
-    int acc = 0, acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    int acc = 0, acc_phase = 0, lt = 0;
+    const bool stamp = tr && warp == 2 && lane == 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
       const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
       const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
       const int row0 = m0 + quarter * 32;
@@ -291,6 +323,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
       if (KIND != OUT_S32 && p.token_scales != nullptr && row < p.M) s_tok = __ldg(p.token_scales + row);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (stamp && lt < 15) tr[4 + 4 * lt] = gtime();
       const uint32_t t_row =
           tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
 #pragma unroll 1
@@ -306,27 +339,30 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
         }
         const int col0 = n0 + c;
         if (row0 >= p.M || col0 >= p.N) continue;  // warp-uniform
-        if (p.tma_out) {
-          if (lane == 0) bulk_wait_read0();  // previous store finished reading stage_c
+        if (p.tma_out && col0 + 32 <= p.N) {
+          // stage the 32x32 chunk (row = lane, swizzled) and write it back with
+          // coalesced 16-byte stores: each store instruction covers whole rows
+          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
           __syncwarp();
-          epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
-          fence_proxy_async_smem();
+          if (!(p.debug & 1)) store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
           __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmC, stage_c, col0, row0);
-            bulk_commit();
-          }
+        } else if (p.tma_out) {
+          if (row < p.M)
+            epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
+                                 col0, p.N);
         } else if (row < p.M) {
           epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
                                col0, p.N);
         }
       }
+      if (stamp && lt < 15) tr[5 + 4 * lt] = gtime();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
     if (lane == 0) bulk_wait0();
+    if (stamp) tr[63] = gtime();
   } else if (W4) {
     // ===================== INT4 -> INT8 unpack (W4A8) =====================
     // 4 warps.  Packed tile (BN rows x 64 B, K-major, unswizzled) -> int8 tile in
@@ -486,6 +522,8 @@ static int make_tmap_u8(CUtensorMap* tm, const void* base, int64_t rows, int64_t
 }
 
 static int g_num_sms = 0;
+static unsigned long long* g_trace = nullptr;
+static int g_debug = 0;
 
 template <int BN, int KIND, int W4>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
@@ -576,6 +614,8 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
+  p.trace = g_trace;
+  p.debug = g_debug;
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
   {
@@ -620,6 +660,13 @@ using namespace zq;
 extern "C" {
 
 const char* zq_version(void) { return "zq_b200 0.1.0 sm_100a tcgen05-i8"; }
+
+int zq_gemm_set_trace(unsigned long long* buf) {
+  g_trace = buf;
+  const char* e = getenv("ZQ_GEMM_DEBUG");
+  g_debug = e ? atoi(e) : 0;
+  return ZQ_OK;
+}
 
 int zq_igemm_s32(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
                  int64_t M, int64_t N, int64_t K, int32_t* acc, int64_t ld_acc, void* stream) {

@@ -12,6 +12,8 @@
 #include <string.h>
 
 #include "zq_common.cuh"
+#include "zq_gelu.cuh"
+#include "zq_rowops.h"
 
 namespace zq {
 
@@ -30,87 +32,8 @@ static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStre
 // Row producers: what value each activation element holds before quantization.
 // ---------------------------------------------------------------------------
 struct IdentityOp {
+  static constexpr bool kWarpOk = true;
   __device__ __forceinline__ float operator()(float x) const { return x; }
-};
-
-// scipy.special.erf (scipy 1.18, the reference's erf: tensor.py:15, :83) is the
-// Cephes ndtr.c algorithm: odd symmetry, a (4,5) rational in x^2 on |x| <= 1,
-// and 1 - erfc(x) above, with erfc = exp(-x^2) * P8(x)/Q8(x) (x < 8) or
-// exp(-x^2) * R5(x)/S6(x).  Restated here op for op (round-to-nearest, no
-// contraction) so the f64 result matches scipy bit for bit; this matters for
-// x << 0, where 1 + erf(x) cancels and the last bits of erf survive into the
-// float32 GeLU.  Verified identical to scipy on 5.5e5 points (tools/erf_check.py).
-__device__ __forceinline__ double polevl_d(double x, const double* c, int n) {
-  double a = c[0];
-  for (int i = 1; i <= n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
-  return a;
-}
-__device__ __forceinline__ double p1evl_d(double x, const double* c, int n) {
-  double a = __dadd_rn(x, c[0]);
-  for (int i = 1; i < n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
-  return a;
-}
-__device__ __forceinline__ double cephes_erf(double x) {
-  const double T[5] = {9.60497373987051638749E0, 9.00260197203842689217E1,
-                       2.23200534594684319226E3, 7.00332514112805075473E3,
-                       5.55923013010394962768E4};
-  const double U[5] = {3.35617141647503099647E1, 5.21357949780152679795E2,
-                       4.59432382970980127987E3, 2.26290000613890934246E4,
-                       4.92673942608635921086E4};
-  const double P[9] = {2.46196981473530512524E-10, 5.64189564831068821977E-1,
-                       7.46321056442269912687E0,   4.86371970985681366614E1,
-                       1.96520832956077098242E2,   5.26445194995477358631E2,
-                       9.34528527171957607540E2,   1.02755188689515710272E3,
-                       5.57535335369399327526E2};
-  const double Q[8] = {1.32281951154744992508E1, 8.67072140885989742329E1,
-                       3.54937778887819891062E2, 9.75708501743205489753E2,
-                       1.82390916687909736289E3, 2.24633760818710981792E3,
-                       1.65666309194161350182E3, 5.57535340817727675546E2};
-  const double R[6] = {5.64189583547755073984E-1, 1.27536670759978104416E0,
-                       5.01905042251180477414E0,  6.16021097993053585195E0,
-                       7.40974269950448939160E0,  2.97886665372100240670E0};
-  const double S[6] = {2.26052863220117276590E0, 9.39603524938001434673E0,
-                       1.20489539808096656605E1, 1.70814450747565897222E1,
-                       9.60896809063285878198E0, 3.36907645100081516050E0};
-  const double kMaxLog = 7.09782712893383996843E2;
-  const bool neg = x < 0.0;
-  const double a = fabs(x);
-  double r;
-  if (a <= 1.0) {
-    const double z = __dmul_rn(a, a);
-    r = __ddiv_rn(__dmul_rn(a, polevl_d(z, T, 4)), p1evl_d(z, U, 5));
-  } else {
-    // erfc(a) for a > 1
-    const double z = -__dmul_rn(a, a);
-    double ec;
-    if (z < -kMaxLog) {
-      ec = 0.0;
-    } else {
-      const double e = exp(z);
-      double p, q;
-      if (a < 8.0) {
-        p = polevl_d(a, P, 8);
-        q = p1evl_d(a, Q, 8);
-      } else {
-        p = polevl_d(a, R, 5);
-        q = p1evl_d(a, S, 6);
-      }
-      ec = __ddiv_rn(__dmul_rn(e, p), q);
-    }
-    r = __dsub_rn(1.0, ec);
-  }
-  return neg ? -r : r;
-}
-
-// tensor.py:76-83: f32( (x64 * 0.5) * (1.0 + erf(x64 * (1/sqrt 2))) ), every op
-// in f64 round-to-nearest (no contraction), one final rounding to f32.
-struct GeluOp {
-  __device__ __forceinline__ float operator()(float x) const {
-    const double kInvSqrt2 = 0x1.6a09e667f3bccp-1;  // 1.0 / math.sqrt(2.0) in Python
-    double x64 = (double)x;
-    double e = cephes_erf(__dmul_rn(x64, kInvSqrt2));
-    return __double2float_rn(__dmul_rn(__dmul_rn(x64, 0.5), __dadd_rn(1.0, e)));
-  }
 };
 
 // ---------------------------------------------------------------------------
@@ -146,6 +69,7 @@ __global__ void __launch_bounds__(1024) rowquant_vec_kernel(
   if (bad && flag) atomicOr(flag, 1);
   amax = block_max_nonneg(amax, red);
   const float s = scale_from_absmax(amax, qm);
+  const float inv = safe_rcp(s);
   if (threadIdx.x == 0) scales[row] = s;
   char4* qr = reinterpret_cast<char4*>(q + row * ld_q);
   float4* yr = y_out ? reinterpret_cast<float4*>(y_out + row * cols) : nullptr;
@@ -154,10 +78,10 @@ __global__ void __launch_bounds__(1024) rowquant_vec_kernel(
     int c = threadIdx.x + i * blockDim.x;
     if (c < cols4) {
       char4 o;
-      o.x = (signed char)quantize_exact(v[i].x, s, qm);
-      o.y = (signed char)quantize_exact(v[i].y, s, qm);
-      o.z = (signed char)quantize_exact(v[i].z, s, qm);
-      o.w = (signed char)quantize_exact(v[i].w, s, qm);
+      o.x = (signed char)quantize_fast(v[i].x, s, inv, qm);
+      o.y = (signed char)quantize_fast(v[i].y, s, inv, qm);
+      o.z = (signed char)quantize_fast(v[i].z, s, inv, qm);
+      o.w = (signed char)quantize_fast(v[i].w, s, inv, qm);
       qr[c] = o;
       if (yr) yr[c] = v[i];
     }
@@ -539,6 +463,21 @@ __global__ void __launch_bounds__(256) ln_quant_kernel(
   }
 }
 
+// Uniform-tree test on a host plan: 2^k equal leaves of 64..128 elements.
+static bool plan_uniform(const PairwisePlan& p, int* E_out, int* nchains_out) {
+  if (p.n < 256) return false;
+  const int L = p.leaf_len[0];
+  if (L % 8 != 0 || L < 64 || L > 128) return false;
+  for (int i = 1; i < p.nleaves; ++i)
+    if (p.leaf_len[i] != L) return false;
+  if (p.nleaves & (p.nleaves - 1)) return false;
+  const int nch = 8 * p.nleaves;
+  if (nch < 32 || nch > 512) return false;  // <= 8 warps x 2 chains per lane
+  *E_out = L / 8;
+  *nchains_out = nch;
+  return true;
+}
+
 struct PlanCache {
   int n = -1;
   PairwisePlan plan;
@@ -560,6 +499,13 @@ int zq_quantize_tokenwise(const float* x, int64_t rows, int64_t cols, int64_t ld
   ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "activations must be (tokens x dim), got (%lld, %lld)",
                (long long)rows, (long long)cols);
   ZQ_CHECK_ARG(ld_x >= cols && ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimensions");
+  if (cols % 4 == 0 && ld_x % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+      launch_tok_quant(x, rows, cols, ld_x, qmax_of(bits), q, ld_q, token_scales, flag,
+                       as_stream(stream)) == ZQ_OK) {
+    ZQ_LAUNCH_CHECK("token-wise quantize launch");
+    return ZQ_OK;
+  }
   return launch_rowquant(x, rows, cols, ld_x, bits, IdentityOp{}, nullptr, q, ld_q, token_scales,
                          flag, as_stream(stream));
 }
@@ -570,6 +516,13 @@ int zq_gelu_quantize(const float* x, int64_t rows, int64_t cols, int64_t ld_x, i
   ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
   ZQ_CHECK_ARG(rows >= 1 && cols >= 1, ZQ_ERR_USAGE, "activations must be (tokens x dim)");
   ZQ_CHECK_ARG(ld_x >= cols && ld_q >= cols && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad leading dimensions");
+  if (gelu_out == nullptr && cols % 4 == 0 && ld_x % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+      launch_gelu_quant(x, rows, cols, ld_x, qmax_of(bits), q, ld_q, token_scales, flag,
+                        as_stream(stream)) == ZQ_OK) {
+    ZQ_LAUNCH_CHECK("gelu quantize launch");
+    return ZQ_OK;
+  }
   return launch_rowquant(x, rows, cols, ld_x, bits, GeluOp{}, gelu_out, q, ld_q, token_scales,
                          flag, as_stream(stream));
 }
@@ -680,6 +633,16 @@ int zq_layer_norm_quantize(const float* x, const float* residual, const float* g
     g_plan_cache.n = (int)cols;
   }
   const PairwisePlan& plan = g_plan_cache.plan;
+  int E = 0, nch = 0;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (plan_uniform(plan, &E, &nch) && cols % 4 == 0 && al16(x) && al16(residual) && al16(gamma) &&
+      al16(beta) && al16(ln_out) && al16(q) &&
+      launch_ln_quant_uniform(x, residual, gamma, beta, rows, cols, plan.nleaves, plan.leaf_len[0],
+                              eps, qmax_of(bits), ln_out, q, ld_q, token_scales, flag,
+                              as_stream(stream)) == ZQ_OK) {
+    ZQ_LAUNCH_CHECK("layer_norm_quantize (uniform) launch");
+    return ZQ_OK;
+  }
   size_t smem = sizeof(float) * (cols + 2 * (size_t)plan.nleaves + 2);
   static bool attr_set = false;
   if (!attr_set) {

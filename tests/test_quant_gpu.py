@@ -236,3 +236,38 @@ def test_gelu_digest_and_large(zq, golden_meta):
     qa = igemm.gelu_quantize(x, 8)
     q_ref, s_ref = O.gelu_quantize(x, 8)
     assert same_bits(h(qa.values), q_ref) and same_bits(h(qa.token_scales), s_ref)
+
+
+@pytest.mark.parametrize("std", [0.3, 1.0, 3.0, 10.0])
+def test_gelu_quantize_fast_path_exact(zq, std):
+    """The q/scale-only GeLU path (fp32 bracket + exact f64 fallback) must equal
+    quantize(gelu_f64(x)) bit for bit, including heavy negative tails (< -3,
+    where the reference's 1 + erf cancellation rules) and zero rows."""
+    _, igemm = zq
+    rng = np.random.default_rng(int(std * 10))
+    for (t, d) in [(512, 3072), (64, 4096), (16, 24576), (300, 1024)]:
+        x = (rng.standard_normal((t, d)) * std).astype(F32)
+        x[0] = 0.0
+        x[1, : d // 2] = -abs(x[1, : d // 2]) - 3.0
+        x[2] = -np.abs(x[2])
+        qa = igemm.gelu_quantize(x, 8)
+        q_ref, s_ref = O.gelu_quantize(x, 8)
+        assert same_bits(h(qa.token_scales), s_ref), (t, d, std)
+        assert same_bits(h(qa.values), q_ref), (t, d, std)
+
+
+def test_ln_uniform_and_generic_paths_agree(zq):
+    """Balanced-tree (uniform) and generic plan LN kernels vs numpy for widths
+    around the uniform/non-uniform boundary."""
+    _, igemm = zq
+    rng = np.random.default_rng(21)
+    for d in (256, 512, 768, 1024, 2048, 3072, 4096, 6144, 640, 1000, 1536, 2304):
+        x = (rng.standard_normal((37, d)) * 2 + 0.5).astype(F32)
+        g = (1 + 0.1 * rng.standard_normal(d)).astype(F32)
+        b = (0.1 * rng.standard_normal(d)).astype(F32)
+        ln = torch.empty((37, d), dtype=torch.float32, device="cuda")
+        qa = igemm.layer_norm_quantize(x, g, b, 8, ln_out=ln)
+        ref = O.layer_norm_numpy(x, g, b)
+        assert same_bits(h(ln), ref), d
+        q_ref, s_ref = O.quantize_activation_tokenwise(ref, 8)
+        assert same_bits(h(qa.values), q_ref) and same_bits(h(qa.token_scales), s_ref), d

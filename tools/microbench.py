@@ -13,6 +13,16 @@ from paper_2206_01861_b200 import igemm, quant  # noqa: E402
 from tools.timing import graph_time, sets_needed  # noqa: E402
 
 
+def calib_benches(res):
+    """Harness calibration: a torch elementwise op of known traffic."""
+    for n in (4096 * 768, 4096 * 3072):
+        ns = sets_needed(8 * n)
+        X = [torch.randn(n, device="cuda") for _ in range(ns)]
+        Y = [torch.empty(n, device="cuda") for _ in range(ns)]
+        sec = graph_time([(lambda i=i: torch.mul(X[i], 2.0, out=Y[i])) for i in range(ns)])
+        res[f"calib_torch_mul_{n}"] = {"us": sec * 1e6, "GBps": 8 * n / sec / 1e9}
+
+
 def quant_benches(res):
     for (t, d) in [(4096, 768), (4096, 3072), (16, 6144), (2048, 6144), (16, 24576)]:
         nb = 5 * t * d
@@ -76,6 +86,7 @@ def main():
     res = {}
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("all", "quant"):
+        calib_benches(res)
         quant_benches(res)
     if which in ("all", "gemm"):
         gemm_benches(res)
