@@ -135,6 +135,15 @@ int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t 
                             const float* amax, int bits, int8_t* q, int64_t ld_q,
                             float* token_scales, void* stream);
 
+/* Float attention of the block (transformer.py:413-440) for `batch` packed
+ * sequences: qkv [batch*seq, ld_qkv] holds q | k | v (heads*head_dim columns
+ * each), ctx [batch*seq, ld_ctx].  tcgen05 kind::tf32 with a 3-term hi/lo split
+ * (~fp32 accuracy; tolerance parity).  Supports seq <= 128, head_dim == 64;
+ * returns ZQ_ERR_UNSUPPORTED otherwise. */
+int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads,
+                     int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
+                     void* stream);
+
 /* Diagnostics: when buf != NULL, subsequent GEMM launches record per-CTA
  * %globaltimer stamps into buf[cta*64 + slot] (slot 0 entry, 1 setup done,
  * 2+4t / 3+4t MMA start / last operands landed for local tile t, 4+4t / 5+4t

@@ -264,19 +264,40 @@ def _act_mode_for(precision: PrecisionConfig, site: str, layer: int, static_scal
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int, causal: bool,
-              batch: int = 1) -> torch.Tensor:
-    """transformer.py:413-440 on device, float32, for `batch` sequences packed as
-    [batch*t, d] rows (each sequence attends only to itself)."""
+              batch: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """transformer.py:413-440 on device, float, for `batch` sequences packed as
+    [batch*t, d] rows (each sequence attends only to itself).
+
+    q, k, v are column views of one [T, 3d] qkv buffer (as produced by the fused
+    QKV GEMM): then the fused tcgen05 kernel (zq_attention_f32, 3xTF32 split,
+    ~fp32 accuracy) runs for t <= 128, head_dim 64; other shapes use torch's
+    float32 scaled-dot-product attention."""
     bt, d = q.shape
     t = bt // batch
     dh = d // num_heads
+    scale = float(np.float32(1.0 / math.sqrt(dh)))
+    fused = (t <= 128 and dh == 64 and q.stride(1) == 1 and k.data_ptr() == q.data_ptr() + 4 * d
+             and v.data_ptr() == q.data_ptr() + 8 * d and q.stride(0) == k.stride(0) == v.stride(0))
+    if fused:
+        ctx = out if out is not None else torch.empty((bt, d), dtype=torch.float32, device=q.device)
+        lib = N.load()
+        rc = lib.zq_attention_f32(q.data_ptr(), q.stride(0), batch, t, num_heads, dh, int(causal),
+                                  scale, ctx.data_ptr(), ctx.stride(0), N.stream_ptr())
+        if rc == N.ZQ_OK:
+            return ctx
+        if rc != N.ZQ_ERR_UNSUPPORTED:
+            N.check(rc)
 
     def heads(z):
         return z.reshape(batch, t, num_heads, dh).transpose(1, 2)
 
     ctx = torch.nn.functional.scaled_dot_product_attention(
-        heads(q), heads(k), heads(v), is_causal=causal, scale=float(np.float32(1.0 / math.sqrt(dh))))
-    return ctx.transpose(1, 2).reshape(bt, d).contiguous()
+        heads(q), heads(k), heads(v), is_causal=causal, scale=scale)
+    ctx = ctx.transpose(1, 2).reshape(bt, d)
+    if out is not None:
+        out.copy_(ctx)
+        return out
+    return ctx.contiguous()
 
 
 def _linear_site(x, w: QuantizedMatrix, bias, am):
@@ -402,8 +423,8 @@ class EncoderEngine:
         for blk in self.blocks:
             self._linear(xq, sx, blk.w_qkv, blk.b_qkv, B["qkv"])
             qkv = B["qkv"]
-            B["ctx"].copy_(attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads,
-                                     self.causal, self.batch))
+            attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads, self.causal,
+                      self.batch, out=B["ctx"])
             self._tok_quant(B["ctx"], B["cq"], B["sc"])
             self._linear(B["cq"], B["sc"], blk.w_o, blk.b_o, B["attn"])
             self._ln_quant(x, B["attn"], blk.ln1_gamma, blk.ln1_beta, B["h"], B["hq"], B["sh"])
