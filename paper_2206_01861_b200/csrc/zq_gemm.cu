@@ -414,6 +414,186 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2, int8 weights): a cluster of 2 CTAs
+// computes a 256 x BN tile.  CTA r holds A rows [128r, 128r+128) and B rows
+// [r*BN/2, (r+1)*BN/2) of the pair tile in its own smem; the leader (r = 0)
+// issues M=256 MMAs that read both CTAs' smem and write each CTA's TMEM (its
+// 128 rows x BN columns).  Per SM and K-block the smem traffic drops from
+// 2 x (16 + BN) KB to 2 x (16 + BN/2) KB, which is what bounds the 1-CTA kernel
+// (TMA writes + tensor-core reads share the smem port).
+//   full_bar   (leader): 2 arrivals (one per CTA producer) + both CTAs' TMA bytes
+//   empty_bar  (each)  : multicast tcgen05.commit from the leader
+//   tfull_bar  (each)  : multicast commit after a tile's last MMA
+//   tempty_bar (leader): 2 x kNumEpiWarps arrivals (both CTAs' epilogue warps)
+// ---------------------------------------------------------------------------
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int A_BYTES = BLOCK_M * BLOCK_K;
+  static constexpr int B_BYTES = (BN / 2) * BLOCK_K;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 192 * 1024 / STAGE_BYTES > 8 ? 8 : 192 * 1024 / STAGE_BYTES;
+  static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 4;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int NUM_THREADS = (2 + kNumEpiWarps) * 32;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+};
+
+template <int BN, int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
+    zq_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParams p) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sC = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + Cfg::EPI_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + STAGES;
+  uint64_t* tfull_bar = bars + 2 * STAGES;
+  uint64_t* tempty_bar = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 2);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 2 * kNumEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = p.num_k_blocks;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    int stage = 0, phase = 0;
+    for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+      const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
+      const int n0 = (tile % p.num_n_tiles) * BN + rank * (BN / 2);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (lane == 0) {
+          const uint32_t fb = leader_addr(&full_bar[stage]);
+          if (leader)
+            mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+          else
+            mbar_arrive_cluster(fb);
+          tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+          tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, n0);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader only) =====================
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_i8(2 * BLOCK_M, BN);
+      int stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BLOCK_K / 32; ++k)
+              mma_i8_cg2(d_tmem, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32),
+                         idesc, (kb | k) != 0);
+            mma_commit_mc2(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) mma_commit_mc2(&tfull_bar[acc], 0x3);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (both CTAs, own 128 rows) =====================
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int COLS = BN / 2;
+    uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
+    int acc = 0, acc_phase = 0;
+    for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+      const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
+      const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
+      const int row0 = m0 + quarter * 32;
+      const int row = row0 + lane;
+      float s_tok = p.static_scale;
+      if (KIND != OUT_S32 && p.token_scales != nullptr && row < p.M) s_tok = __ldg(p.token_scales + row);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
+#pragma unroll 1
+      for (int c = 0; c < COLS; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c, r);
+        tmem_ld_wait();
+        if (c + 32 == COLS) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty_bar[acc]));
+        }
+        const int col0 = n0 + c;
+        if (row0 >= p.M || col0 >= p.N) continue;
+        if (p.tma_out && col0 + 32 <= p.N) {
+          epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
+          __syncwarp();
+          store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
+          __syncwarp();
+        } else if (row < p.M) {
+          epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
+                               col0, p.N);
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
 // Standalone epilogue over an int32 accumulator (TP path) and the weight-only
 // FullAct GEMM (sequential f32 order, tensor.py:37-56).
 // ---------------------------------------------------------------------------
@@ -541,6 +721,22 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   return ZQ_OK;
 }
 
+template <int BN, int KIND>
+static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p,
+                          cudaStream_t st) {
+  using Cfg = Gemm2Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zq_gemm2_kernel<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
+    attr = true;
+  }
+  const int pairs = p.num_tiles < g_num_sms / 2 ? p.num_tiles : g_num_sms / 2;
+  zq_gemm2_kernel<BN, KIND><<<2 * pairs, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
+  ZQ_LAUNCH_CHECK("tcgen05 cta-pair gemm launch");
+  return ZQ_OK;
+}
+
 template <int KIND, int W4>
 static int launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                           const CUtensorMap& tc, GemmParams p, cudaStream_t st) {
@@ -596,6 +792,46 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  // CTA-pair path for int8 weights when there are enough 256-row tiles to fill
+  // the machine (ZQ_GEMM_PAIR=0 disables, =1 forces where legal)
+  static int pair_mode = -1;
+  if (pair_mode < 0) {
+    const char* e = getenv("ZQ_GEMM_PAIR");
+    pair_mode = e ? atoi(e) : 2;
+  }
+  if (w_bits == 8 && pair_mode != 0) {
+    const int64_t mp = (M + 2 * BLOCK_M - 1) / (2 * BLOCK_M);
+    int bn2 = 0;
+    if (mp * ((N + 255) / 256) >= g_num_sms / 2 || (pair_mode == 1 && N >= 256)) bn2 = 256;
+    else if (mp * ((N + 127) / 128) >= g_num_sms / 2 || pair_mode == 1) bn2 = 128;
+    if (bn2) {
+      CUtensorMap ta, tb;
+      int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+      rc = make_tmap_u8(&tb, wq, N, K, ld_w, BLOCK_K, bn2 / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+      p.M = (int)M;
+      p.N = (int)N;
+      p.K = (int)K;
+      p.trace = nullptr;
+      p.debug = 0;
+      const int esz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : 4;
+      p.tma_out = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0) && ((p.ld_out * esz) % 16 == 0) &&
+                  (p.row_scales == nullptr || (reinterpret_cast<uintptr_t>(p.row_scales) & 15) == 0) &&
+                  (p.bias == nullptr || (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0);
+      p.num_n_tiles = (int)((N + bn2 - 1) / bn2);
+      p.num_tiles = (int)mp * p.num_n_tiles;
+      p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, p, st) : launch_gemm2_t<128, KK>(ta, tb, p, st))
+      switch (kind) {
+        case OUT_S32: return ZQ_G2(OUT_S32);
+        case OUT_F32: return ZQ_G2(OUT_F32);
+        case OUT_F16: return ZQ_G2(OUT_F16);
+        default: return ZQ_G2(OUT_BF16);
+      }
+#undef ZQ_G2
+    }
   }
   const int bn = pick_bn(M, N);
   CUtensorMap ta, tb;
