@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = GemmCfg<BN, W4>;
   constexpr int STAGES = Cfg::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // no static smem: the dynamic window is 1024-aligned (checked below), and using
+  // it without an integer round trip keeps the epilogue staging on LDS/STS
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;                              // STAGES x [128 rows x 128 B]
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;      // STAGES x [BN rows x 128 B]
   uint8_t* sP = smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES);  // W4: STAGES x [BN x 64 B]
@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
 
   if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * 64] = gtime();
   if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B needs 1024-byte aligned stages
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     if (p.tma_out) prefetch_tmap(&tmC);
@@ -444,9 +445,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
                     const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // no static smem: the dynamic window is 1024-aligned (checked below), and using
+  // it without an integer round trip keeps the epilogue staging on LDS/STS
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sC = smem + STAGES * Cfg::STAGE_BYTES;
@@ -464,6 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B needs 1024-byte aligned stages
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
@@ -695,6 +697,28 @@ static int make_tmap_u8(CUtensorMap* tm, const void* base, int64_t rows, int64_t
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld", (int)r,
+              (long long)rows, (long long)cols, (long long)ld_bytes);
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+// Shared with zq_attention.cu: 2-D float32 tensor map (row-major, ld in bytes).
+int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
+                  int box_cols, int box_rows, CUtensorMapSwizzle sw) {
+  if (!get_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ZQ_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32) failed (%d): rows=%lld cols=%lld ld=%lld", (int)r,
               (long long)rows, (long long)cols, (long long)ld_bytes);
     return ZQ_ERR_CUDA;
   }

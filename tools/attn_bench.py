@@ -1,0 +1,31 @@
+"""Time the fused attention kernel at the BERT-base shape (32 x 128 tokens,
+12 heads x 64) with CUDA-graph replay over rotating buffers > L2."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2206_01861_b200 import transformer as T  # noqa: E402
+from tools.timing import graph_time, sets_needed  # noqa: E402
+
+
+def main():
+    batch, seq, heads, dh = 32, 128, 12, 64
+    d = heads * dh
+    t = batch * seq
+    nb = t * 3 * d * 4 + t * d * 4
+    ns = sets_needed(nb)
+    Q = [torch.randn(t, 3 * d, device="cuda") for _ in range(ns)]
+    C = [torch.empty(t, d, device="cuda") for _ in range(ns)]
+    for causal in (False, True):
+        fs = [(lambda i=i: T.attention(Q[i][:, :d], Q[i][:, d:2 * d], Q[i][:, 2 * d:], heads, causal, batch,
+                                       out=C[i])) for i in range(ns)]
+        sec = graph_time(fs)
+        print(json.dumps({"kernel": "attention", "causal": causal, "us": round(sec * 1e6, 2),
+                          "GBps": round(nb / sec / 1e9, 1)}))
+
+
+if __name__ == "__main__":
+    main()
