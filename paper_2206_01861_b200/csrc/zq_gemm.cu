@@ -463,6 +463,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtime();
 
   if (warp == 0 && lane == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B needs 1024-byte aligned stages
@@ -484,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int nkb = p.num_k_blocks;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -513,14 +516,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     // ===================== MMA issuer (leader only) =====================
     if (leader) {
       constexpr uint32_t idesc = make_idesc_i8(2 * BLOCK_M, BN);
-      int stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+      int stage = 0, phase = 0, acc = 0, acc_phase = 0, lt = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (tr && lane == 0 && lt < 15) tr[2 + 4 * lt] = gtime();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (tr && lane == 0 && lt < 15 && kb == nkb - 1) tr[3 + 4 * lt] = gtime();
           if (lane == 0) {
             const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
             const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
@@ -550,8 +555,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
     uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
-    int acc = 0, acc_phase = 0;
-    for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+    int acc = 0, acc_phase = 0, lt = 0;
+    const bool stamp = tr && warp == 2 && lane == 0;
+    for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
       const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
       const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
       const int row0 = m0 + quarter * 32;
@@ -560,6 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
       if (KIND != OUT_S32 && p.token_scales != nullptr && row < p.M) s_tok = __ldg(p.token_scales + row);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (stamp && lt < 15) tr[4 + 4 * lt] = gtime();
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
 #pragma unroll 1
       for (int c = 0; c < COLS; c += 32) {
@@ -574,20 +581,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
         const int col0 = n0 + c;
         if (row0 >= p.M || col0 >= p.N) continue;
         if (p.tma_out && col0 + 32 <= p.N) {
-          epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
+          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
           __syncwarp();
-          store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
+          if (!(p.debug & 1)) store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
           __syncwarp();
         } else if (row < p.M) {
           epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
                                col0, p.N);
         }
       }
+      if (stamp && lt < 15) tr[5 + 4 * lt] = gtime();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (stamp) tr[63] = gtime();
   }
   tc_fence_before();
   __syncthreads();
@@ -838,8 +847,8 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.M = (int)M;
       p.N = (int)N;
       p.K = (int)K;
-      p.trace = nullptr;
-      p.debug = 0;
+      p.trace = g_trace;
+      p.debug = g_debug;
       const int esz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : 4;
       p.tma_out = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0) && ((p.ld_out * esz) % 16 == 0) &&
                   (p.row_scales == nullptr || (reinterpret_cast<uintptr_t>(p.row_scales) & 15) == 0) &&
