@@ -144,11 +144,32 @@ int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int h
                      int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
                      void* stream);
 
+/* GPT decode: scatter the k and v column blocks of the
+ * fused QKV output qkv [batch*rows_per_seq, ld_qkv] (q | k | v, dmodel_local
+ * columns each) into f32 caches [batch, max_ctx, dmodel_local] at rows
+ * pos[b] .. pos[b]+rows_per_seq-1 (pos: device int32 [batch]).  The reference
+ * recomputes the context each step (evaluate.py:96-98); cached rows are
+ * bit-identical to the recomputed ones. */
+int zq_kv_append(const float* qkv, int64_t ld_qkv, int batch, int rows_per_seq, int dmodel_local,
+                 const int32_t* pos, float* kcache, float* vcache, int64_t max_ctx, void* stream);
+
+/* One-token-per-sequence attention against the caches (transformer.py:413-440
+ * for the last query row): ctx[b, h] = softmax(q.K^T * scale) V over the first
+ * lens[b] cached tokens (device int32).  head_dim % 32 == 0, <= 256. */
+int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, const float* vcache,
+                            int64_t max_ctx, int batch, int heads, int head_dim,
+                            const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
+                            void* stream);
+
 /* Diagnostics: when buf != NULL, subsequent GEMM launches record per-CTA
  * %globaltimer stamps into buf[cta*64 + slot] (slot 0 entry, 1 setup done,
  * 2+4t / 3+4t MMA start / last operands landed for local tile t, 4+4t / 5+4t
  * epilogue start / end, 63 epilogue exit).  Not thread-safe; tooling only. */
 int zq_gemm_set_trace(unsigned long long* buf);
+
+/* Diagnostics: mode 20 makes zq_attention_f32 record 8 %globaltimer stamps per
+ * CTA (phase boundaries) into ctx instead of its output; 0 = normal. */
+int zq_attention_debug(int mode);
 
 #ifdef __cplusplus
 }

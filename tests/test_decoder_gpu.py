@@ -1,0 +1,103 @@
+"""GPU: GPT prefill + cached decode (paper_2206_01861_b200.decoder) vs the
+oracle recomputing the whole causal context with the reference block
+(transformer.py:443-486, evaluate.py:96-98 recomputation).  Attention is float
+on both sides, so hidden states are compared with the block tolerance; the
+greedy tokens must agree."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lowbit_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def make_weights(rng, d, f):
+    w = {n: rng.gaussian(s, std=0.02) for n, s in (
+        ("w_q", (d, d)), ("w_k", (d, d)), ("w_v", (d, d)), ("w_o", (d, d)),
+        ("w_h4h", (f, d)), ("w_4hh", (d, f)))}
+    for n, s in (("b_q", d), ("b_k", d), ("b_v", d), ("b_o", d), ("b_h4h", f), ("b_4hh", d)):
+        w[n] = rng.gaussian((s,), std=0.02)
+    for n in ("ln1", "ln2"):
+        w[f"{n}_gamma"] = (1.0 + rng.gaussian((d,), std=0.1)).astype(np.float32)
+        w[f"{n}_beta"] = rng.gaussian((d,), std=0.1)
+    return w
+
+
+def oracle_hidden(ids_row, emb, qbs, heads, gamma, beta):
+    x = emb[ids_row]
+    for qb in qbs:
+        x = O.block_forward(x, qb, heads, True, "int8")
+    return O.layer_norm(x, gamma, beta)
+
+
+@pytest.mark.parametrize("mbits,fbits", [(8, 8), (8, 4)])
+def test_prefill_and_cached_decode_match_recompute(mbits, fbits):
+    from paper_2206_01861_b200 import transformer as T
+    from paper_2206_01861_b200.decoder import DecoderEngine, GPTConfig
+
+    d, heads, f, V, L, g = 256, 4, 1024, 512, 2, 16
+    cfg = GPTConfig("tiny", L, d, heads, f, V, mbits, fbits, g)
+    rng = O.Rng(7)
+    ws = [make_weights(rng, d, f) for _ in range(L)]
+    emb = rng.gaussian((V, d), std=1.0)
+    prec = T.PrecisionConfig.from_scheme("W8A8" if fbits == 8 else "W4/8A8", group_count=g)
+    blocks = []
+    for w in ws:
+        w = dict(w, num_heads=heads)
+        blocks.append(T.quantize_block(w, prec))
+    qbs = [O.quantize_block(w, mbits, fbits, g) for w in ws]
+    batch, Tp = 3, 9
+    ids = np.random.default_rng(0).integers(0, V, (batch, Tp))
+    eng = DecoderEngine(cfg, batch, max_ctx=32, blocks=blocks, embedding=emb)
+    gamma, beta = eng.final_gamma.cpu().numpy(), eng.final_beta.cpu().numpy()
+    first = eng.prefill(ids).cpu().numpy()
+    h_prefill = eng._buffers(batch * Tp)["out"][:batch].cpu().numpy()
+    toks = [first]
+    hs = []
+    for _ in range(3):
+        toks.append(eng.step().cpu().numpy())
+        hs.append(eng._buffers(batch)["out"][:batch].cpu().numpy())
+    eng.check_finite()
+    full = np.concatenate([ids, np.stack(toks, 1)], axis=1)
+    for b in range(batch):
+        ref = oracle_hidden(full[b, :Tp], emb, qbs, heads, gamma, beta)
+        assert rel(h_prefill[b], ref[-1]) < TOL, (b, rel(h_prefill[b], ref[-1]))
+        for s in range(3):
+            ref = oracle_hidden(full[b, :Tp + 1 + s], emb, qbs, heads, gamma, beta)
+            assert rel(hs[s][b], ref[-1]) < TOL, (b, s, rel(hs[s][b], ref[-1]))
+            logits = ref[-1] @ emb.T
+            assert int(np.argmax(logits)) == int(full[b, Tp + 1 + s]), (b, s)
+
+
+def test_decode_attention_vs_torch():
+    from paper_2206_01861_b200 import _native as N
+
+    for dh, heads in ((64, 4), (96, 3), (256, 2)):
+        batch, max_ctx = 3, 40
+        dl = dh * heads
+        torch.manual_seed(dh)
+        kc = torch.randn(batch, max_ctx, dl, device="cuda")
+        vc = torch.randn(batch, max_ctx, dl, device="cuda")
+        q = torch.randn(batch, 3 * dl, device="cuda")
+        lens = torch.tensor([1, 17, 40], dtype=torch.int32, device="cuda")
+        ctx = torch.empty(batch, dl, device="cuda")
+        scale = 1.0 / dh ** 0.5
+        N.call("zq_decode_attention_f32", q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), max_ctx,
+               batch, heads, dh, lens.data_ptr(), scale, ctx.data_ptr(), ctx.stride(0), N.stream_ptr())
+        for b in range(batch):
+            n = int(lens[b])
+            qh = q[b, :dl].double().view(heads, 1, dh)
+            k = kc[b, :n].double().view(n, heads, dh).transpose(0, 1)
+            v = vc[b, :n].double().view(n, heads, dh).transpose(0, 1)
+            p = torch.softmax(qh @ k.transpose(1, 2) * scale, -1)
+            ref = (p @ v).reshape(dl)
+            assert torch.allclose(ctx[b].double(), ref, rtol=1e-5, atol=1e-5), (dh, b)
