@@ -1,6 +1,7 @@
 """Benchmark driver (contract in the task statement; workload = BASELINE.json configs[1]).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload bert|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bert|c1|gpt3-350m|gptj-6b|neox-20b]
 
 Default workload: BERT-base full INT8 W8A8 encoder forward, batch 32 x seq 128,
 random-init weights (Gaussian 0.02), synthetic token ids, 12 post-LN blocks
@@ -338,12 +339,261 @@ def run_ours(args, rank: int, world: int, dist):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# GPT workloads (BASELINE configs 2-4): prefill + greedy decode with KV cache
+# ---------------------------------------------------------------------------
+
+GPT_RUNS = {
+    # name: (batch, prompt tokens, new tokens)
+    "gpt3-350m": (8, 1024, 16),
+    "gptj-6b": (16, 128, 128),
+    "neox-20b": (16, 128, 128),
+}
+
+
+def _gpt_ref_worker(args):
+    """Reference algorithm (oracle port) on one sequence of `t` tokens through one
+    block of the named GPT shape: returns seconds."""
+    name, t, seed = args
+    import numpy as np
+
+    from oracle import lowbit_oracle as O
+    from paper_2206_01861_b200.decoder import CONFIGS
+
+    cfg = CONFIGS[name]
+    O.use_reference_cost_igemm(True)
+    d, f = cfg.dim, cfg.ffn
+    rng = np.random.default_rng(seed)  # fast generator: only the block's cost is measured
+    w = {n: (rng.standard_normal(s, dtype=np.float32) * np.float32(0.02)) for n, s in (
+        ("w_q", (d, d)), ("w_k", (d, d)), ("w_v", (d, d)), ("w_o", (d, d)),
+        ("w_h4h", (f, d)), ("w_4hh", (d, f)))}
+    for n, s in (("b_q", d), ("b_k", d), ("b_v", d), ("b_o", d), ("b_h4h", f), ("b_4hh", d),
+                 ("ln1_beta", d), ("ln2_beta", d)):
+        w[n] = np.zeros(s, np.float32)
+    w["ln1_gamma"] = np.ones(d, np.float32)
+    w["ln2_gamma"] = np.ones(d, np.float32)
+    qb = O.quantize_block(w, cfg.mhsa_bits, cfg.ffc_bits, cfg.groups)
+    x = O.Rng(seed + 1).gaussian((t, d), std=0.5)
+    t0 = time.perf_counter()
+    O.block_forward(x, qb, cfg.heads, True, "int8")
+    return time.perf_counter() - t0
+
+
+def gpt_cpu_sample(name: str, cores: int):
+    """Reference CPU throughput estimate for the generation workload: the
+    reference recomputes the full context per generated token (evaluate.py:96-98),
+    so a generated token costs one causal forward over the context.  Sample: one
+    block over a 16-token sequence per core (bounded), scaled linearly in tokens
+    (the int64 igemm dominates and is linear in tokens) and x layers."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    from paper_2206_01861_b200.decoder import CONFIGS
+
+    cfg = CONFIGS[name]
+    batch, prompt, new = GPT_RUNS[name]
+    ts = 8
+    with ProcessPoolExecutor(max_workers=1) as ex:  # one core: a GPT-scale block is ~GBs of host RAM
+        secs = list(ex.map(_gpt_ref_worker, [(name, ts, 1)]))
+    cores = 1
+    per_tok_layer = statistics.median(secs) / ts
+    # tokens processed by recomputation: sum over steps of the context length
+    ctx_tokens = batch * sum(prompt + i for i in range(new))
+    total_s = per_tok_layer * cfg.layers * ctx_tokens / cores
+    value = batch * new / total_s
+    sample = (f"1 process x 1 {cfg.name} block over {ts} tokens (reference numpy algorithm, int64 "
+              f"igemm); x{cfg.layers} layers, x full-context recomputation per generated token "
+              f"(evaluate.py:96-98), extrapolated")
+    return value, sample, cores
+
+
+def run_gpt(args, rank: int, world: int, dist):
+    import numpy as np
+    import torch
+
+    from paper_2206_01861_b200.decoder import CONFIGS, DecoderEngine
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    name = args.workload
+    cfg = CONFIGS[name]
+    batch, prompt, new = GPT_RUNS[name]
+    tp = (None, rank, world) if world > 1 else None
+    eng = DecoderEngine(cfg, batch, prompt + new, seed=0, tp=tp)
+    ids_host = torch.from_numpy(np.random.default_rng(0).integers(0, cfg.vocab, (batch, prompt))).pin_memory()
+    ids_dev = ids_host.cuda()
+    out_host = torch.empty((batch, new), dtype=torch.int64).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def generate(ids):
+        toks = [eng.prefill(ids).clone()]
+        for _ in range(new - 1):
+            toks.append(eng.step().clone())
+        return torch.stack(toks, 1)
+
+    for _ in range(args.warmup):
+        generate(ids_dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    pre_t, dec_t, tot_t = [], [], []
+    barrier()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, m, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record(stream)
+            toks = [eng.prefill(ids_dev).clone()]
+            m.record(stream)
+            for _ in range(new - 1):
+                toks.append(eng.step().clone())
+            b.record(stream)
+            pre_t.append((a, m))
+            dec_t.append((m, b))
+        barrier()
+    prefill_s = sum(x.elapsed_time(y) for x, y in pre_t) * 1e-3
+    decode_s = sum(x.elapsed_time(y) for x, y in dec_t) * 1e-3
+    total = prefill_s + decode_s
+    eng.check_finite()
+    # end to end: host ids -> tokens back on the host
+    barrier()
+    e2e = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out_host.copy_(generate(ids_host), non_blocking=True)
+        b.record(stream)
+        e2e.append((a, b))
+    barrier()
+    e2e_s = sum(x.elapsed_time(y) for x, y in e2e) * 1e-3
+    if dist is not None:
+        t = torch.tensor([total, prefill_s, decode_s, e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total, prefill_s, decode_s, e2e_s = (float(v) for v in t)
+    if rank != 0:
+        return
+    # roofline of the decode step: int8 weight bytes streamed per step vs HBM
+    peaks, basis = load_peaks()
+    wbytes = 0
+    for blk in eng.blocks:
+        for wn in ("w_qkv", "w_o", "w_h4h", "w_4hh"):
+            w = getattr(blk, wn)
+            wbytes += w.rows * w.ld * (w.bits / 8)
+    step_s = decode_s / (args.steps * (new - 1))
+    achieved = wbytes / step_s / 1e9
+    toks = batch * new * args.steps
+    cores = len(os.sched_getaffinity(0))
+    cpu_val, cpu_sample, cores = gpt_cpu_sample(name, cores)
+    line = {
+        "metric": f"{cfg.name} greedy generation throughput", "value": toks / total, "unit": "tok/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (random-init weights, random prompt ids)",
+        "config": {"workload": f"{cfg.name}: batch {batch}, prompt {prompt}, {new} new tokens (greedy, KV cache)",
+                   "layers": cfg.layers, "hidden": cfg.dim, "heads": cfg.heads, "ffn": cfg.ffn,
+                   "weight_bits": [cfg.mhsa_bits, cfg.ffc_bits], "weight_groups": cfg.groups,
+                   "parallelism": f"tp{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB memset) before each generation"},
+        "prefill_tok_per_s": batch * prompt * args.steps / prefill_s,
+        "decode_ms_per_token": 1000 * step_s,
+        "e2e": {"value": toks / e2e_s, "unit": "tok/s", "h2d_bytes_per_step": int(ids_host.numel() * 8),
+                "d2h_bytes_per_step": int(out_host.numel() * 8)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": "decode step: int8 weight streaming of all quantized linears (per rank)",
+                     "peak_basis": f"{basis} HBM copy bandwidth (MEASURED_PEAKS.json)"},
+        "cpu_baseline": {"value": cpu_val, "unit": "tok/s", "cores": cores, "kind": "port", "sample": cpu_sample},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_c1(args, rank: int, world: int, dist):
+    """BASELINE configs[0]: one W8A8 quantized linear 768->3072 over 32x128 tokens
+    (fp32 in, f32 out), activation quantization included; metric = TOPS."""
+    import torch
+
+    from paper_2206_01861_b200 import _native as N
+    from paper_2206_01861_b200 import igemm, quant
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    t, k, n, g = 4096, 768, 3072, 48
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    sets = []
+    for _ in range(8):  # rotating inputs (8 x 22 MB > L2)
+        x = torch.randn((t, k), generator=gen, device="cuda")
+        sets.append(x)
+    w = quant.quantize_weight_groupwise(torch.randn((n, k), generator=gen, device="cuda") * 0.02, g, 8)
+    bias = torch.zeros(n, device="cuda")
+    out = torch.empty((t, n), device="cuda")
+    q = quant.padded_int8(t, k)
+    s = torch.empty(t, device="cuda")
+    fl = quant.FiniteFlag()
+    wp, ldw, wb = w.weight_operand()
+
+    def step(x):
+        N.call("zq_quantize_tokenwise", x.data_ptr(), t, k, k, 8, q.data_ptr(), q.stride(0), s.data_ptr(),
+               fl.ptr, N.stream_ptr())
+        N.call("zq_linear", q.data_ptr(), q.stride(0), s.data_ptr(), 0.0, wp, ldw, wb, w.row_scales().data_ptr(),
+               bias.data_ptr(), t, n, k, out.data_ptr(), out.stride(0), N.OUT_F32, N.stream_ptr())
+
+    for i in range(args.warmup):
+        step(sets[i % 8])
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    ev = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for i in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(sets[i % 8])
+            b.record(stream)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+    sec = sum(a.elapsed_time(b) for a, b in ev) * 1e-3 / args.steps
+    ops = 2 * t * k * n
+    x_host = torch.randn((t, k)).pin_memory()
+    o_host = torch.empty((t, n)).pin_memory()
+    torch.cuda.synchronize()
+    ev = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        xd = x_host.cuda(non_blocking=True)
+        o_host.copy_(igemm.quantized_linear(xd, w, bias, igemm.DynamicAct(8)), non_blocking=True)
+        b.record(stream)
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    e2e = sum(a.elapsed_time(b) for a, b in ev) * 1e-3 / args.steps
+    if rank != 0:
+        return
+    peaks, basis = load_peaks()
+    line = {"metric": "ZeroQuant W8A8 quantized linear throughput (incl. token-wise activation quantization)",
+            "value": ops / sec / 1e12, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * sec, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[0]: 4096 tokens x 768 -> 3072, groups 48, f32 in/out",
+                       "l2": "8 rotating 12.6 MB inputs"},
+            "e2e": {"value": ops / e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": t * k * 4,
+                    "d2h_bytes_per_step": t * n * 4},
+            "roofline": {"bound": "tensor", "achieved": ops / sec / 1e12, "peak": 2 * peaks["bf16_tflops"],
+                         "unit": "TFLOP/s", "frac": ops / sec / 1e12 / (2 * peaks["bf16_tflops"]), "traffic": None,
+                         "peak_basis": f"2 x {basis} bf16 dense"},
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bert", choices=["bert", "c1"] + sorted(GPT_RUNS))
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -360,7 +610,12 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
-    run_ours(args, rank, world, dist)
+    if args.workload == "bert":
+        run_ours(args, rank, world, dist)
+    elif args.workload == "c1":
+        run_c1(args, rank, world, dist)
+    else:
+        run_gpt(args, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()
 

@@ -604,6 +604,159 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
   if (warp == 1) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
 }
 
+
+// ---------------------------------------------------------------------------
+// Skinny (decode) GEMM, M <= 64 tokens, int8 weights: weight-streaming bound.
+// Swap-AB: the MMA's M=128 side is 128 weight rows (output channels), its N side
+// the MP (32 / 64) padded token rows, so D^T[n, m] sits in TMEM lane n.  Split-K
+// over a cluster of S CTAs (S = 1..8) fills the machine: CTA r of the cluster
+// accumulates k-blocks [r*nkb/S, (r+1)*nkb/S) of the same 128 weight rows, writes
+// its int32 partial to its own smem, and after a cluster barrier reduces 128/S of
+// the rows across all S partials through distributed shared memory (exact: int32
+// addition is order-free) and applies the dequant epilogue for them.
+// ---------------------------------------------------------------------------
+constexpr int kSkStages = 4;
+
+template <int MP>
+struct SkinnyCfg {
+  static constexpr int A_BYTES = 128 * BLOCK_K;   // weight tile
+  static constexpr int B_BYTES = MP * BLOCK_K;    // token tile
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int PART_BYTES = MP * 128 * 4; // int32 partial [MP][128]
+  static constexpr int SMEM_BYTES = kSkStages * STAGE_BYTES + PART_BYTES + 256;
+};
+
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ int32_t dsmem_ld_s32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int MP, int KIND>
+__global__ void __launch_bounds__(128, 1)
+    zq_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                          const GemmParams p, int S) {
+  using Cfg = SkinnyCfg<MP>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kSkStages * Cfg::A_BYTES;
+  int32_t* part = reinterpret_cast<int32_t*>(smem + kSkStages * Cfg::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSkStages * Cfg::STAGE_BYTES + Cfg::PART_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + kSkStages;
+  uint64_t* done_bar = bars + 2 * kSkStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kSkStages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = (int)cluster_ctarank();
+  const int n0 = (blockIdx.x / S) * 128;
+  const int nkb = p.num_k_blocks;
+  const int kb0 = (int)(((int64_t)nkb * r) / S), kb1 = (int)(((int64_t)nkb * (r + 1)) / S);
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int st = 0; st < kSkStages; ++st) {
+      mbar_init(&full_bar[st], 1);
+      mbar_init(&empty_bar[st], 1);
+    }
+    mbar_init(done_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, MP < 32 ? 32 : MP);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    int stage = 0, phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&empty_bar[stage], phase ^ 1);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        tma_load_2d(sA + stage * Cfg::A_BYTES, &tmW, &full_bar[stage], kb * BLOCK_K, n0);
+        tma_load_2d(sB + stage * Cfg::B_BYTES, &tmX, &full_bar[stage], kb * BLOCK_K, 0);
+      }
+      __syncwarp();
+      if (++stage == kSkStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_i8(128, MP);
+    int stage = 0, phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full_bar[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+        const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BLOCK_K / 32; ++k)
+          mma_i8(tmem, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32), idesc,
+                 (kb != kb0 || k != 0) ? 1u : 0u);
+        mma_commit(&empty_bar[stage]);
+      }
+      __syncwarp();
+      if (++stage == kSkStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (lane == 0) {
+      if (kb1 > kb0) mma_commit(done_bar);
+      else mbar_arrive(done_bar);  // empty split: contributes zeros
+    }
+    __syncwarp();
+  }
+  // ---- partial: TMEM (lane = weight row) -> smem [MP][128] ----
+  mbar_wait(done_bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+#pragma unroll
+  for (int c = 0; c < MP; c += 32) {
+    uint32_t v[32];
+    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) part[(c + j) * 128 + row] = kb1 > kb0 ? (int32_t)v[j] : 0;
+  }
+  tc_fence_before();
+  cluster_sync();
+  // ---- cluster reduction + epilogue for rows [r*RP, (r+1)*RP) ----
+  const int RP = 128 / S;
+  const uint32_t pbase = smem_u32(part);
+  for (int it = threadIdx.x; it < MP * RP; it += 128) {
+    const int m = it / RP, nl = r * RP + it % RP;
+    const int n = n0 + nl;
+    if (m >= p.M || n >= p.N) continue;
+    const uint32_t off = pbase + (uint32_t)(m * 128 + nl) * 4;
+    int32_t acc = 0;
+    for (int s2 = 0; s2 < S; ++s2) acc += dsmem_ld_s32(dsmem_map(off, (uint32_t)s2));
+    const int64_t o = (int64_t)m * p.ld_out + n;
+    if (KIND == OUT_S32) {
+      reinterpret_cast<int32_t*>(p.out)[o] = acc;
+    } else {
+      const float st = p.token_scales ? __ldg(p.token_scales + m) : p.static_scale;
+      float f = __fmul_rn(__fmul_rn(__int2float_rn(acc), st), __ldg(p.row_scales + n));
+      if (p.bias) f = __fadd_rn(f, __ldg(p.bias + n));
+      if (KIND == OUT_F32) reinterpret_cast<float*>(p.out)[o] = f;
+      else if (KIND == OUT_F16) reinterpret_cast<__half*>(p.out)[o] = __float2half_rn(f);
+      else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(f);
+    }
+  }
+  cluster_sync();  // peers may still be reading this CTA's partial
+  if (warp == 1) tmem_dealloc(tmem, MP < 32 ? 32 : MP);
+}
+
 // ---------------------------------------------------------------------------
 // Standalone epilogue over an int32 accumulator (TP path) and the weight-only
 // FullAct GEMM (sequential f32 order, tensor.py:37-56).
@@ -796,6 +949,71 @@ static int pick_bn(int64_t M, int64_t N) {
   return 64;
 }
 
+template <int MP, int KIND>
+static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmParams p, int S,
+                           cudaStream_t st) {
+  using Cfg = SkinnyCfg<MP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zq_gemm_skinny_kernel<MP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(p.num_n_tiles * S), 1, 1);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, zq_gemm_skinny_kernel<MP, KIND>, tw, tx, p, S);
+  if (e != cudaSuccess) {
+    set_error("skinny gemm launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+// Split-K degree: the largest S (<= 8) whose grid still fits one wave of two
+// CTAs per SM (a partial second wave costs more than the extra split saves) and
+// leaves every split >= 2 k-blocks.
+static int pick_split(int n_tiles, int nkb) {
+  int S = 1;
+  while (S < 8 && n_tiles * S * 2 <= 2 * g_num_sms && nkb / (2 * S) >= 2) S *= 2;
+  return S;
+}
+
+static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int64_t M,
+                       int64_t N, int64_t K, int kind, GemmParams p, cudaStream_t st) {
+  const int MP = M <= 32 ? 32 : 64;
+  CUtensorMap tw, tx;
+  int rc = make_tmap_u8(&tw, wq, N, K, ld_w, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_tmap_u8(&tx, xq, M, K, ld_x, BLOCK_K, MP, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.num_n_tiles = (int)((N + 127) / 128);
+  p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+  p.num_tiles = p.num_n_tiles;
+  const int S = pick_split(p.num_n_tiles, p.num_k_blocks);
+#define ZQ_SK(KK) (MP == 32 ? launch_skinny_t<32, KK>(tw, tx, p, S, st) : launch_skinny_t<64, KK>(tw, tx, p, S, st))
+  switch (kind) {
+    case OUT_S32: return ZQ_SK(OUT_S32);
+    case OUT_F32: return ZQ_SK(OUT_F32);
+    case OUT_F16: return ZQ_SK(OUT_F16);
+    default: return ZQ_SK(OUT_BF16);
+  }
+#undef ZQ_SK
+}
+
 static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits,
                        int64_t M, int64_t N, int64_t K, int kind, GemmParams p,
                        cudaStream_t st) {
@@ -826,6 +1044,14 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
+  // decode-sized token counts: weight-streaming skinny kernel (ZQ_GEMM_SKINNY=0 disables)
+  static int skinny_mode = -1;
+  if (skinny_mode < 0) {
+    const char* e = getenv("ZQ_GEMM_SKINNY");
+    skinny_mode = e ? atoi(e) : 1;
+  }
+  if (w_bits == 8 && M <= 64 && skinny_mode != 0)
+    return gemm_skinny(xq, ld_x, wq, ld_w, M, N, K, kind, p, st);
   // CTA-pair path for int8 weights when there are enough 256-row tiles to fill
   // the machine (ZQ_GEMM_PAIR=0 disables, =1 forces where legal)
   static int pair_mode = -1;

@@ -193,3 +193,23 @@ def test_scale_linearity_power_of_two(zq):
     base = h(igemm.dequant_epilogue(acc, s, w))
     doubled = h(igemm.dequant_epilogue(acc, s * F32(2.0), w))
     assert np.array_equal(doubled, base * F32(2.0))
+
+
+@pytest.mark.parametrize("shape", [(1, 4096, 4096), (16, 4096, 12288), (33, 16384, 4096), (64, 768, 3072),
+                                   (7, 6144, 3000), (16, 24576, 6144), (2, 200, 300)])
+def test_skinny_decode_gemm_exact(zq, shape):
+    """M <= 64 runs the split-K swap-AB kernel (cluster DSMEM reduction): the int32
+    accumulators and the fused f32 epilogue must stay bit-exact."""
+    quant, igemm = zq
+    t, d, n = shape
+    rng = np.random.default_rng(sum(shape))
+    xv = rng.integers(-127, 128, (t, d)).astype(np.int8)
+    wv = rng.integers(-127, 128, (n, d)).astype(np.int8)
+    xa, wm = make_qact(quant, xv, scales=rng.random(t).astype(F32) + 0.01), make_qmat(quant, wv, scales=(0.003,))
+    acc = igemm.igemm(xa, wm)
+    ref_acc = O.igemm(xv, wv)
+    assert np.array_equal(h(acc.acc), ref_acc), shape
+    bias = rng.standard_normal(n).astype(F32)
+    out = igemm.fused_linear(xa, wm, bias)
+    ref = O.dequant_epilogue(ref_acc, h(xa.token_scales), np.full(n, F32(0.003)), bias)
+    assert bits_eq(h(out), ref), shape

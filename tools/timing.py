@@ -25,10 +25,12 @@ def graph_time(launches, reps: int = 5, warm: int = 3) -> float:
                 f()
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
+    inner = max(1, -(-20 // len(launches)))  # >= 20 launches per replay: amortise the graph launch
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        for f in launches:
-            f()
+        for _ in range(inner):
+            for f in launches:
+                f()
     g.replay()
     torch.cuda.synchronize()
     out = []
@@ -38,6 +40,6 @@ def graph_time(launches, reps: int = 5, warm: int = 3) -> float:
         g.replay()
         b.record()
         torch.cuda.synchronize()
-        out.append(a.elapsed_time(b) * 1e-3 / len(launches))
+        out.append(a.elapsed_time(b) * 1e-3 / (inner * len(launches)))
     out.sort()
     return out[len(out) // 2]
