@@ -9,6 +9,8 @@
 // with causal attention and token-wise activation scales the cached k / v rows
 // are exactly the rows that recomputation would produce, so caching changes no
 // value — only float attention (tolerance parity) runs here.
+#include <string.h>
+
 #include "zq_common.cuh"
 
 namespace zq {
@@ -30,25 +32,54 @@ __global__ void kv_append_kernel(const float* __restrict__ qkv, int64_t ld_qkv, 
   }
 }
 
-// One CTA (256 threads) per (sequence, head).  dh % 32 == 0, dh <= 256.
-//  1. scores: 8 lanes per key (4 keys per warp step), float4 chunks, xor-reduce;
-//  2. softmax over lens[b] scores in smem (block max / sum);
-//  3. ctx = sum_j p_j v_j: G key groups of dh/4 threads (one float4 of dims
-//     each), partial sums combined through smem.
-__global__ void __launch_bounds__(256) decode_attention_kernel(
+// Flash-decoding: a cluster of C CTAs per (sequence, head); CTA c takes the
+// keys [c*chunk, (c+1)*chunk) below lens[b] and produces a partial
+// (max m_c, sum l_c, unnormalised o_c = sum_j e^(s_j - m_c) v_j); after a cluster
+// barrier each CTA combines dims [c*dh/C, (c+1)*dh/C) of all C partials through
+// distributed shared memory:  o = sum_c o_c e^(m_c - M) / sum_c l_c e^(m_c - M).
+// 256 threads; scores: 8 lanes per key (4 keys per warp step, float4 chunks,
+// xor-reduce); P.V: G = 256/(dh/4) key groups of dh/4 threads (float4 of dims).
+constexpr int kDecThreads = 256;
+
+__device__ __forceinline__ uint32_t dsm_map(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float dsm_ld_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kDecThreads) decode_attention_kernel(
     const float* __restrict__ q, int64_t ld_q, const float* __restrict__ kc,
     const float* __restrict__ vc, int64_t max_ctx, int heads, int dh,
-    const int32_t* __restrict__ lens, float scale, float* __restrict__ ctx, int64_t ld_ctx) {
+    const int32_t* __restrict__ lens, float scale, float* __restrict__ ctx, int64_t ld_ctx,
+    int C, int chunk) {
   extern __shared__ float dsm[];
   __shared__ float red[32];
-  const int b = blockIdx.x / heads, h = blockIdx.x % heads;
+  __shared__ float stat[2];  // m_c, l_c
+  const int c = (int)cta_rank_in_cluster();
+  const int bh = blockIdx.x / C;
+  const int b = bh / heads, h = bh % heads;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int dl = heads * dh;
   const int len = lens[b];
-  float* sq = dsm;            // [dh]
-  float* sc = dsm + 256;      // [max_ctx] scores -> probabilities
-  float* part = sc + max_ctx; // [G][dh] partial outputs
-  for (int i = tid; i < dh; i += 256) sq[i] = q[(int64_t)b * ld_q + h * dh + i];
+  const int j0 = c * chunk, j1 = min(len, j0 + chunk);
+  const int G = kDecThreads / (dh >> 2);
+  float* sq = dsm;                 // [dh]
+  float* sc = dsm + 256;           // [chunk]
+  float* po = sc + chunk;          // [G][dh] partial outputs; row 0 = o_c after the reduce
+  for (int i = tid; i < dh; i += kDecThreads) sq[i] = q[(int64_t)b * ld_q + h * dh + i];
   __syncthreads();
 
   const int d4 = dh >> 2;
@@ -56,38 +87,46 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(
   const float* vb = vc + (int64_t)b * max_ctx * dl + h * dh;
   {
     const int sub = lane >> 3, l8 = lane & 7;
-    for (int j0 = warp * 4; j0 < len; j0 += 32) {
-      const int j = j0 + sub;
+#pragma unroll 2
+    for (int jj = j0 + warp * 4; jj < j1; jj += 4 * (kDecThreads / 32)) {
+      const int j = jj + sub;
       float acc = 0.0f;
-      if (j < len) {
+      if (j < j1) {
+        // issue every load of the key row first (dh <= 256: <= 8 float4 per lane)
         const float4* kr = reinterpret_cast<const float4*>(kb + (int64_t)j * dl);
-        for (int c = l8; c < d4; c += 8) {
-          const float4 kv = __ldg(kr + c);
-          const float4 qv = *reinterpret_cast<const float4*>(sq + 4 * c);
-          acc = __fmaf_rn(qv.x, kv.x, acc);
-          acc = __fmaf_rn(qv.y, kv.y, acc);
-          acc = __fmaf_rn(qv.z, kv.z, acc);
-          acc = __fmaf_rn(qv.w, kv.w, acc);
+        float4 kv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          kv[i] = (l8 + 8 * i < d4) ? __ldg(kr + l8 + 8 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (l8 + 8 * i < d4) {
+            const float4 qv = *reinterpret_cast<const float4*>(sq + 4 * (l8 + 8 * i));
+            acc = __fmaf_rn(qv.x, kv[i].x, acc);
+            acc = __fmaf_rn(qv.y, kv[i].y, acc);
+            acc = __fmaf_rn(qv.z, kv[i].z, acc);
+            acc = __fmaf_rn(qv.w, kv[i].w, acc);
+          }
         }
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      if (l8 == 0 && j < len) sc[j] = __fmul_rn(acc, scale);
+      if (l8 == 0 && j < j1) sc[j - j0] = __fmul_rn(acc, scale);
     }
   }
   __syncthreads();
   float mx = -INFINITY;
-  for (int j = tid; j < len; j += 256) mx = fmaxf(mx, sc[j]);
+  for (int j = tid; j < j1 - j0; j += kDecThreads) mx = fmaxf(mx, sc[j]);
   mx = warp_max(mx);
   if (lane == 0) red[warp] = mx;
   __syncthreads();
   mx = red[0];
 #pragma unroll
-  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  for (int w = 1; w < kDecThreads / 32; ++w) mx = fmaxf(mx, red[w]);
   __syncthreads();
   float sum = 0.0f;
-  for (int j = tid; j < len; j += 256) {
+  for (int j = tid; j < j1 - j0; j += kDecThreads) {
     const float e = expf(sc[j] - mx);
     sc[j] = e;
     sum += e;
@@ -96,31 +135,52 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (lane == 0) red[warp] = sum;
   __syncthreads();
-  sum = 0.0f;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) sum += red[w];
-  const float inv = 1.0f / sum;
-
-  const int G = 256 / d4;  // key groups
-  const int g = tid / d4, c = tid % d4;
+  if (tid == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < kDecThreads / 32; ++w) t += red[w];
+    stat[0] = mx;  // -inf for an empty chunk
+    stat[1] = t;
+  }
+  const int g = tid / d4, cc = tid % d4;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
   if (g < G) {
-    for (int j = g; j < len; j += G) {
-      const float p = sc[j];
-      const float4 v = __ldg(reinterpret_cast<const float4*>(vb + (int64_t)j * dl) + c);
-      o.x = __fmaf_rn(p, v.x, o.x);
-      o.y = __fmaf_rn(p, v.y, o.y);
-      o.z = __fmaf_rn(p, v.z, o.z);
-      o.w = __fmaf_rn(p, v.w, o.w);
+#pragma unroll 8
+    for (int j = j0 + g; j < j1; j += G) {
+      const float pj = sc[j - j0];
+      const float4 v = __ldg(reinterpret_cast<const float4*>(vb + (int64_t)j * dl) + cc);
+      o.x = __fmaf_rn(pj, v.x, o.x);
+      o.y = __fmaf_rn(pj, v.y, o.y);
+      o.z = __fmaf_rn(pj, v.z, o.z);
+      o.w = __fmaf_rn(pj, v.w, o.w);
     }
-    *reinterpret_cast<float4*>(part + g * dh + 4 * c) = o;
+    *reinterpret_cast<float4*>(po + g * dh + 4 * cc) = o;
   }
   __syncthreads();
-  for (int i = tid; i < dh; i += 256) {
-    float s = 0.0f;
-    for (int gg = 0; gg < G; ++gg) s += part[gg * dh + i];
-    ctx[(int64_t)b * ld_ctx + h * dh + i] = s * inv;
+  for (int i = tid; i < dh; i += kDecThreads) {
+    float t = 0.0f;
+    for (int gg = 0; gg < G; ++gg) t += po[gg * dh + i];
+    po[i] = t;  // row 0 of po = o_c
   }
+  cluster_barrier();
+  // combine dims [c*dh/C, (c+1)*dh/C) across the cluster
+  const int da = (c * dh) / C, db = ((c + 1) * dh) / C;
+  const uint32_t stat_a = smem_u32(stat), po_a = smem_u32(po);
+  float M = -INFINITY;
+  for (int r = 0; r < C; ++r) M = fmaxf(M, dsm_ld_f32(dsm_map(stat_a, r)));
+  float L = 0.0f;
+  for (int r = 0; r < C; ++r) {
+    const float mr = dsm_ld_f32(dsm_map(stat_a, r));
+    if (mr != -INFINITY) L += dsm_ld_f32(dsm_map(stat_a + 4, r)) * expf(mr - M);
+  }
+  for (int i = da + tid; i < db; i += kDecThreads) {
+    float t = 0.0f;
+    for (int r = 0; r < C; ++r) {
+      const float mr = dsm_ld_f32(dsm_map(stat_a, r));
+      if (mr != -INFINITY) t += dsm_ld_f32(dsm_map(po_a + 4 * i, r)) * expf(mr - M);
+    }
+    ctx[(int64_t)b * ld_ctx + h * dh + i] = t / L;
+  }
+  cluster_barrier();  // keep this CTA's partial alive until every peer has read it
 }
 
 }  // namespace zq
@@ -151,8 +211,13 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
   ZQ_CHECK_ARG(batch >= 1 && heads >= 1 && max_ctx >= 1, ZQ_ERR_SHAPE, "bad decode attention shape");
   ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
                "decode attention supports head_dim % 32 == 0 and <= 256");
-  const int G = 256 / (head_dim / 4);
-  const size_t smem = sizeof(float) * (256 + (size_t)max_ctx + (size_t)G * head_dim);
+  // context chunks per (sequence, head): split until ~4 CTAs per SM are in flight,
+  // at most 8 (portable cluster), keeping >= 32 keys per chunk
+  int C = 1;
+  while (C < 8 && (int64_t)batch * heads * C < 4 * 148 && max_ctx / (2 * C) >= 32) C *= 2;
+  const int chunk = (int)((max_ctx + C - 1) / C);
+  const int G = kDecThreads / (head_dim / 4);
+  const size_t smem = sizeof(float) * (256 + (size_t)chunk + (size_t)G * head_dim);
   ZQ_CHECK_ARG(smem <= 200 * 1024, ZQ_ERR_UNSUPPORTED, "context too long for decode attention");
   static bool attr = false;
   if (!attr) {
@@ -160,9 +225,25 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
                          200 * 1024);
     attr = true;
   }
-  decode_attention_kernel<<<batch * heads, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      q, ld_q, kcache, vcache, max_ctx, heads, head_dim, lens, scale, ctx, ld_ctx);
-  ZQ_LAUNCH_CHECK("decode attention launch");
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(batch * heads * C), 1, 1);
+  cfg.blockDim = dim3(kDecThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_attention_kernel, q, ld_q, kcache, vcache, max_ctx,
+                                     heads, head_dim, lens, scale, ctx, ld_ctx, C, chunk);
+  if (e != cudaSuccess) {
+    set_error("decode attention launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }
 

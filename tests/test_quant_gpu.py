@@ -245,11 +245,12 @@ def test_gelu_quantize_fast_path_exact(zq, std):
     where the reference's 1 + erf cancellation rules) and zero rows."""
     _, igemm = zq
     rng = np.random.default_rng(int(std * 10))
-    for (t, d) in [(512, 3072), (64, 4096), (16, 24576), (300, 1024)]:
+    for (t, d) in [(512, 3072), (64, 4096), (16, 24576), (300, 1024), (3, 16384), (1, 4096), (5, 6004)]:
         x = (rng.standard_normal((t, d)) * std).astype(F32)
-        x[0] = 0.0
-        x[1, : d // 2] = -abs(x[1, : d // 2]) - 3.0
-        x[2] = -np.abs(x[2])
+        if t >= 3:
+            x[0] = 0.0
+            x[1, : d // 2] = -abs(x[1, : d // 2]) - 3.0
+            x[2] = -np.abs(x[2])
         qa = igemm.gelu_quantize(x, 8)
         q_ref, s_ref = O.gelu_quantize(x, 8)
         assert same_bits(h(qa.token_scales), s_ref), (t, d, std)
