@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(256, 1)
   ts[1] = gtime();
 
   // ---- 1. TMA: Q, K, V boxes of this (sequence, head) ----
+  pdl_trigger();
+  pdl_wait();  // the QKV GEMM output is ready (and the previous ctx reader is done)
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar[0], 6 * 128 * 128);
     const int row0 = b * seq;
@@ -369,8 +371,12 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     attr = true;
   }
-  attention_kernel<<<batch * heads, 256, kAttSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, g_att_dbg);
-  ZQ_LAUNCH_CHECK("attention launch");
+  const cudaError_t e = launch_kernel(attention_kernel, dim3(batch * heads), dim3(256), kAttSmem,
+                                      reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads,
+                                      heads * head_dim, causal, scale, ctx, ld_ctx, g_att_dbg);
+  if (e != cudaSuccess) {
+    set_error("attention launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }

@@ -16,6 +16,46 @@ namespace zq {
 // ---------------------------------------------------------------------------
 void set_error(const char* fmt, ...);
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every hot-path kernel is launched with
+// programmatic stream serialization, calls pdl_trigger() early (the next kernel
+// may start its prologue: barrier init, TMEM alloc, tensor-map prefetch, weight
+// TMA loads) and pdl_wait() before touching anything a previous kernel writes
+// or reads (griddepcontrol.wait returns once the preceding grid has completed
+// and its memory is visible).  ZQ_PDL=0 disables the launch attribute.
+// ---------------------------------------------------------------------------
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t st, unsigned cluster_x, Args... args) {
+  cudaLaunchConfig_t cfg;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 #define ZQ_CHECK_ARG(cond, code, ...)     \
   do {                                    \
     if (!(cond)) {                        \

@@ -20,6 +20,8 @@ __global__ void kv_append_kernel(const float* __restrict__ qkv, int64_t ld_qkv, 
                                  int dl, const int32_t* __restrict__ pos, float* __restrict__ kc,
                                  float* __restrict__ vc, int64_t max_ctx, int64_t total4) {
   const int d4 = dl >> 2;
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int c4 = (int)(i % d4);
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_attention_kernel(
   extern __shared__ float dsm[];
   __shared__ float red[32];
   __shared__ float stat[2];  // m_c, l_c
+  pdl_trigger();
+  pdl_wait();
   const int c = (int)cta_rank_in_cluster();
   const int bh = blockIdx.x / C;
   const int b = bh / heads, h = bh % heads;
@@ -198,9 +202,13 @@ int zq_kv_append(const float* qkv, int64_t ld_qkv, int batch, int rows_per_seq, 
   const int64_t total4 = (int64_t)batch * rows_per_seq * (dmodel_local / 4);
   int blocks = (int)((total4 + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  kv_append_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      qkv, ld_qkv, rows_per_seq, dmodel_local, pos, kcache, vcache, max_ctx, total4);
-  ZQ_LAUNCH_CHECK("kv append launch");
+  const cudaError_t e = launch_kernel(kv_append_kernel, dim3(blocks), dim3(256), 0,
+                                      reinterpret_cast<cudaStream_t>(stream), 1, qkv, ld_qkv,
+                                      rows_per_seq, dmodel_local, pos, kcache, vcache, max_ctx, total4);
+  if (e != cudaSuccess) {
+    set_error("kv append launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }
 
@@ -225,21 +233,9 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
                          200 * 1024);
     attr = true;
   }
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)(batch * heads * C), 1, 1);
-  cfg.blockDim = dim3(kDecThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_attention_kernel, q, ld_q, kcache, vcache, max_ctx,
-                                     heads, head_dim, lens, scale, ctx, ld_ctx, C, chunk);
+  cudaError_t e = launch_kernel(decode_attention_kernel, dim3(batch * heads * C), dim3(kDecThreads), smem,
+                                reinterpret_cast<cudaStream_t>(stream), C, q, ld_q, kcache, vcache,
+                                max_ctx, heads, head_dim, lens, scale, ctx, ld_ctx, C, chunk);
   if (e != cudaSuccess) {
     set_error("decode attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;

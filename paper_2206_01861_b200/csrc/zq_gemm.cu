@@ -236,18 +236,30 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
   const int nkb = p.num_k_blocks;
   unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
   if (tr && threadIdx.x == 0) tr[1] = gtime();
+  pdl_trigger();
   if (warp == 0) {
     // ===================== TMA producer =====================
     // whole warp walks the loop (keeps the warp converged for the final
-    // __syncthreads); lane 0 issues.
+    // __syncthreads); lane 0 issues.  The first tile's weight stages are
+    // requested before the grid dependency resolves (weights are constant).
     int stage = 0, phase = 0;
+    const int pre = (!W4 && (int)blockIdx.x < p.num_tiles) ? (nkb < STAGES ? nkb : STAGES) : 0;
+    if (lane == 0)
+      for (int kb = 0; kb < pre; ++kb) {
+        mbar_arrive_expect_tx(&full_bar[kb], Cfg::STAGE_BYTES);
+        tma_load_2d(sB + kb * Cfg::B_BYTES, &tmB, &full_bar[kb], kb * BLOCK_K,
+                    ((int)blockIdx.x % p.num_n_tiles) * BN);
+      }
+    pdl_wait();
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
       const int n0 = (tile % p.num_n_tiles) * BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
-          if (W4) {
+          if (tile == (int)blockIdx.x && kb < pre) {
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full_bar[stage], kb * BLOCK_K, m0);
+          } else if (W4) {
             // packed weights -> staging (praw_bar); the unpack warps write the
             // int8 tile and add 4 arrivals on full_bar
             mbar_arrive_expect_tx(&praw_bar[stage], Cfg::P_BYTES);
@@ -309,6 +321,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
     // half of the tile's columns.  Per 32x32 chunk: tcgen05.ld -> dequant in
     // registers (thread = row) -> swizzled smem staging -> one TMA store per warp
     // (coalesced, clipped at the M/N edges by the tensor map).
+    pdl_wait();  // token scales come from the previous kernel; `out` may still be read by it
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
@@ -488,9 +501,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
   const int nkb = p.num_k_blocks;
   if (tr && threadIdx.x == 0) tr[1] = gtime();
 
+  pdl_trigger();
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
+    // weight halves of the first tile's stages go out before the grid dependency
     int stage = 0, phase = 0;
+    const int pre = pair < p.num_tiles ? (nkb < STAGES ? nkb : STAGES) : 0;
+    if (lane == 0)
+      for (int kb = 0; kb < pre; ++kb) {
+        const uint32_t fb = leader_addr(&full_bar[kb]);
+        if (leader)
+          mbar_arrive_expect_tx(&full_bar[kb], 2 * Cfg::STAGE_BYTES);
+        else
+          mbar_arrive_cluster(fb);
+        tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K,
+                        (pair % p.num_n_tiles) * BN + rank * (BN / 2));
+      }
+    pdl_wait();
     for (int tile = pair; tile < p.num_tiles; tile += npairs) {
       const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
       const int n0 = (tile % p.num_n_tiles) * BN + rank * (BN / 2);
@@ -498,12 +525,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = leader_addr(&full_bar[stage]);
-          if (leader)
-            mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
-          else
-            mbar_arrive_cluster(fb);
-          tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
-          tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, n0);
+          if (tile == pair && kb < pre) {
+            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+          } else {
+            if (leader)
+              mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+            else
+              mbar_arrive_cluster(fb);
+            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+            tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, n0);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -551,6 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     }
   } else {
     // ===================== epilogue (both CTAs, own 128 rows) =====================
+    pdl_wait();
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
@@ -675,13 +707,24 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  pdl_trigger();
   if (warp == 0) {
+    // the first kSkStages weight tiles stream in before the grid dependency resolves
     int stage = 0, phase = 0;
+    const int pre = (kb1 - kb0) < kSkStages ? (kb1 - kb0) : kSkStages;
+    if (lane == 0)
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
+        tma_load_2d(sA + i * Cfg::A_BYTES, &tmW, &full_bar[i], (kb0 + i) * BLOCK_K, n0);
+      }
+    pdl_wait();
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&empty_bar[stage], phase ^ 1);
       if (lane == 0) {
-        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-        tma_load_2d(sA + stage * Cfg::A_BYTES, &tmW, &full_bar[stage], kb * BLOCK_K, n0);
+        if (kb - kb0 >= pre) {
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmW, &full_bar[stage], kb * BLOCK_K, n0);
+        }
         tma_load_2d(sB + stage * Cfg::B_BYTES, &tmX, &full_bar[stage], kb * BLOCK_K, 0);
       }
       __syncwarp();
@@ -730,6 +773,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int j = 0; j < 32; ++j) part[(c + j) * 128 + row] = kb1 > kb0 ? (int32_t)v[j] : 0;
   }
   tc_fence_before();
+  pdl_wait();
   cluster_sync();
   // ---- cluster reduction + epilogue for rows [r*RP, (r+1)*RP) ----
   const int RP = 128 / S;
@@ -902,8 +946,12 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     attr = true;
   }
   int grid = p.num_tiles < g_num_sms ? p.num_tiles : g_num_sms;
-  zq_gemm_kernel<BN, KIND, W4><<<grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, tc, p);
-  ZQ_LAUNCH_CHECK("tcgen05 gemm launch");
+  const cudaError_t e = launch_kernel(zq_gemm_kernel<BN, KIND, W4>, dim3(grid), dim3(Cfg::NUM_THREADS),
+                                      Cfg::SMEM_BYTES, st, 1, ta, tb, tc, p);
+  if (e != cudaSuccess) {
+    set_error("tcgen05 gemm launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }
 
@@ -918,8 +966,12 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmPara
     attr = true;
   }
   const int pairs = p.num_tiles < g_num_sms / 2 ? p.num_tiles : g_num_sms / 2;
-  zq_gemm2_kernel<BN, KIND><<<2 * pairs, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
-  ZQ_LAUNCH_CHECK("tcgen05 cta-pair gemm launch");
+  const cudaError_t e = launch_kernel(zq_gemm2_kernel<BN, KIND>, dim3(2 * pairs), dim3(Cfg::NUM_THREADS),
+                                      Cfg::SMEM_BYTES, st, 1, ta, tb, p);
+  if (e != cudaSuccess) {
+    set_error("tcgen05 cta-pair gemm launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }
 
@@ -959,20 +1011,8 @@ static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmPar
                          Cfg::SMEM_BYTES);
     attr = true;
   }
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)(p.num_n_tiles * S), 1, 1);
-  cfg.blockDim = dim3(128, 1, 1);
-  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = S;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, zq_gemm_skinny_kernel<MP, KIND>, tw, tx, p, S);
+  cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND>, dim3(p.num_n_tiles * S), dim3(128),
+                                Cfg::SMEM_BYTES, st, S, tw, tx, p, S);
   if (e != cudaSuccess) {
     set_error("skinny gemm launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;

@@ -11,6 +11,8 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include "zq_common.cuh"
 #include "zq_gelu.cuh"
 #include "zq_rowops.h"
@@ -27,6 +29,15 @@ void set_error(const char* fmt, ...) {
 }
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool pdl_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("ZQ_PDL");
+    mode = e ? atoi(e) : 1;
+  }
+  return mode != 0;
+}
 
 // ---------------------------------------------------------------------------
 // Row producers: what value each activation element holds before quantization.
