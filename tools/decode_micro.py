@@ -56,9 +56,6 @@ def main():
     hl = torch.randn(B, d, device="cuda")
     lg = torch.empty(B, cfg.vocab, device="cuda")
     res["lm_head_f32_cublas"] = graph_time([lambda: torch.matmul(hl, E.t(), out=lg)])
-    keys = torch.zeros(B, dtype=torch.int64, device="cuda")
-    ids = torch.zeros(B, dtype=torch.int64, device="cuda")
-    res["lm_head_argmax_zq"] = graph_time([lambda: N.call("zq_lm_head_argmax_f32", hl.data_ptr(), d, B, E.data_ptr(), cfg.vocab, d, None, keys.data_ptr(), ids.data_ptr(), N.stream_ptr())])
     print(json.dumps({k: (round(v * 1e6, 2) if not k.endswith("GBps") else round(v, 1)) for k, v in res.items()}))
 
 
