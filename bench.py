@@ -201,7 +201,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def build_engine(torch, seed_base: int = 0):
+def build_engine(torch, seed_base: int = 0, lanes: int | None = None):
     from paper_2206_01861_b200 import transformer as T
 
     blocks = [T.random_block(BERT["hidden"], BERT["heads"], 8, 8, BERT["groups"], seed=seed_base + i,
@@ -210,7 +210,8 @@ def build_engine(torch, seed_base: int = 0):
     emb = torch.randn((BERT["vocab"], BERT["hidden"]), generator=gen, device="cuda") * T.INIT_STD
     eng = T.EncoderEngine(blocks=blocks, embedding=emb, final_gamma=torch.ones(BERT["hidden"], device="cuda"),
                           final_beta=torch.zeros(BERT["hidden"], device="cuda"), batch=BERT["batch"],
-                          seq=BERT["seq"], causal=False)
+                          seq=BERT["seq"], causal=False,
+                          lanes=lanes if lanes is not None else int(os.environ.get("ZQ_LANES", "1")))
     return eng
 
 
@@ -220,23 +221,29 @@ def gemm_roofline(torch, eng, peaks, basis):
     from paper_2206_01861_b200 import _native as N
 
     events = []
-    orig = eng._linear
+    engines = eng._sub or [eng]  # lanes run one after another here: per-launch times
+    origs = [e._linear for e in engines]
 
-    def timed_linear(q, s, w, bias, out):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        orig(q, s, w, bias, out)
-        b.record()
-        events.append((a, b, 2 * q.shape[0] * q.shape[1] * w.rows))
+    def make_timed(orig):
+        def timed_linear(q, s, w, bias, out):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            orig(q, s, w, bias, out)
+            b.record()
+            events.append((a, b, 2 * q.shape[0] * q.shape[1] * w.rows))
+        return timed_linear
 
-    eng._linear = timed_linear
+    for e, o in zip(engines, origs):
+        e._linear = make_timed(o)
     try:
         for _ in range(3):
             events.clear()
-            eng._run()
+            for e in engines:
+                e._run()
         torch.cuda.synchronize()
     finally:
-        eng._linear = orig
+        for e, o in zip(engines, origs):
+            e._linear = o
     t = sum(a.elapsed_time(b) * 1e-3 for a, b, _ in events)
     ops = sum(o for _, _, o in events)
     achieved = ops / t / 1e12

@@ -368,10 +368,35 @@ class EncoderEngine:
     seq: int
     causal: bool = False
     use_graph: bool = True
+    lanes: int = 1
     _bufs: dict = field(default_factory=dict, init=False)
     _graph: object = field(default=None, init=False)
+    _sub: list = field(default_factory=list, init=False)
+    _streams: list = field(default_factory=list, init=False)
 
     def __post_init__(self):
+        if self.lanes > 1:
+            # `lanes` independent sub-batches on their own streams: the kernels of
+            # one lane fill the SMs the other lane's latency-bound phases leave idle
+            if self.batch % self.lanes:
+                raise UsageError(f"batch {self.batch} not divisible into {self.lanes} lanes")
+            d = self.embedding.shape[1]
+            sb = self.batch // self.lanes
+            dev = self.embedding.device
+            self._bufs = dict(ids=torch.zeros(self.tokens, dtype=torch.int64, device=dev),
+                              out=torch.empty((self.tokens, d), dtype=torch.float32, device=dev),
+                              flag=torch.zeros(1, dtype=torch.int32, device=dev))
+            for i in range(self.lanes):
+                sub = EncoderEngine(blocks=self.blocks, embedding=self.embedding, final_gamma=self.final_gamma,
+                                    final_beta=self.final_beta, batch=sb, seq=self.seq, causal=self.causal,
+                                    use_graph=False)
+                r0, r1 = i * sb * self.seq, (i + 1) * sb * self.seq
+                sub._bufs["ids"] = self._bufs["ids"][r0:r1]
+                sub._bufs["out"] = self._bufs["out"][r0:r1]
+                sub._bufs["flag"] = self._bufs["flag"]
+                self._sub.append(sub)
+                self._streams.append(torch.cuda.Stream())
+            return
         d = self.embedding.shape[1]
         t = self.batch * self.seq
         f = self.blocks[0].w_h4h.rows
@@ -415,6 +440,15 @@ class EncoderEngine:
                self._bufs["flag"].data_ptr(), N.stream_ptr())
 
     def _run(self):
+        if self._sub:
+            main = torch.cuda.current_stream()
+            for sub, st in zip(self._sub, self._streams):
+                st.wait_stream(main)
+                with torch.cuda.stream(st):
+                    sub._run()
+            for st in self._streams:
+                main.wait_stream(st)
+            return
         B = self._bufs
         d = self.embedding.shape[1]
         torch.index_select(self.embedding, 0, B["ids"], out=B["x"])
