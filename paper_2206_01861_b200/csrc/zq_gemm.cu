@@ -20,6 +20,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cmath>
 #include <mutex>
 
 #include "zq_common.cuh"
@@ -1102,8 +1104,32 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   if (w_bits == 8 && pair_mode != 0) {
     const int64_t mp = (M + 2 * BLOCK_M - 1) / (2 * BLOCK_M);
     int bn2 = 0;
-    if (mp * ((N + 255) / 256) >= g_num_sms / 2 || (pair_mode == 1 && N >= 256)) bn2 = 256;
-    else if (mp * ((N + 127) / 128) >= g_num_sms / 2 || pair_mode == 1) bn2 = 128;
+    static int force_bn2 = -1;
+    if (force_bn2 < 0) {
+      const char* e = getenv("ZQ_GEMM_BN2");
+      force_bn2 = e ? atoi(e) : 0;
+    }
+    if (mp * ((N + 127) / 128) >= g_num_sms / 2 || pair_mode == 1) {
+      // pair tile width from a per-SM cost model (measured on B200): per round a
+      // CTA needs max(MMA, operand delivery through TMA at ~75 GB/s/SM, epilogue
+      // stores at ~35 GB/s/SM); rounds = ceil(tiles / pairs)
+      const int esz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : (kind == OUT_S32 ? 4 : 4);
+      double best = 1e30;
+      for (int cand = 256; cand >= 128; cand -= 128) {
+        if (cand == 256 && N < 256) continue;
+        const double tiles = (double)mp * (double)((N + cand - 1) / cand);
+        const double rounds = std::ceil(tiles / (g_num_sms / 2));
+        const double t_mma = 128.0 * cand * K / 11.1e12;
+        const double t_op = (128.0 + cand / 2) * K / 75e9;
+        const double t_epi = 128.0 * cand * esz / 35e9;
+        const double t = rounds * std::max(t_mma, std::max(t_op, t_epi)) + t_op;
+        if (t < best * 0.97) {  // prefer the wider tile unless the narrower one is clearly faster
+          best = t;
+          bn2 = cand;
+        }
+      }
+    }
+    if (force_bn2 && bn2) bn2 = force_bn2;
     if (bn2) {
       CUtensorMap ta, tb;
       int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
