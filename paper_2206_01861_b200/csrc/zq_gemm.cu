@@ -447,17 +447,24 @@ struct Gemm2Cfg {
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K;
   static constexpr int B_BYTES = (BN / 2) * BLOCK_K;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 192 * 1024 / STAGE_BYTES > 8 ? 8 : 192 * 1024 / STAGE_BYTES;
-  static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 4;
+  // two 32x32 output staging buffers per epilogue warp (bulk TMA stores overlap
+  // the dequant of the next chunk); the operand ring gets the rest of the 227 KB
+  static constexpr int EPI_BYTES = kNumEpiWarps * 2 * 32 * 32 * 4;
+  static constexpr int RING = 232448 - EPI_BYTES - 1024 - 256;
+  static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int NUM_THREADS = (2 + kNumEpiWarps) * 32;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
 template <int BN, int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
     zq_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   // no static smem: the dynamic window is 1024-aligned (checked below), and using
@@ -588,7 +595,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
-    uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
+    uint8_t* stage_c = sC + (warp - 2) * (2 * 32 * 32 * 4);
+    int sbuf = 0;
+    if (p.tma_out && lane == 0) prefetch_tmap(&tmC);
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
@@ -614,11 +623,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
         }
         const int col0 = n0 + c;
         if (row0 >= p.M || col0 >= p.N) continue;
-        if (p.tma_out && col0 + 32 <= p.N) {
-          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
+        if (p.tma_out) {
+          // double-buffered staging: the bulk store of this chunk drains while the
+          // next chunk is dequantised; the tensor map clips the M / N edges
+          uint8_t* sb = stage_c + sbuf * (32 * 32 * 4);
+          if (lane == 0) bulk_wait_read1();  // the store that last used `sb` has read it
           __syncwarp();
-          if (!(p.debug & 1)) store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
+          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, sb, lane);
+          fence_proxy_async_smem();
           __syncwarp();
+          if (lane == 0 && !(p.debug & 1)) {
+            tma_store_2d(&tmC, sb, col0, row0);
+            bulk_commit();
+          }
+          sbuf ^= 1;
         } else if (row < p.M) {
           epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
                                col0, p.N);
@@ -630,6 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait0();  // all output stores complete before exit
     if (stamp) tr[63] = gtime();
   }
   tc_fence_before();
@@ -958,7 +977,7 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 }
 
 template <int BN, int KIND>
-static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p,
+static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, GemmParams p,
                           cudaStream_t st) {
   using Cfg = Gemm2Cfg<BN>;
   static bool attr = false;
@@ -969,7 +988,7 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmPara
   }
   const int pairs = p.num_tiles < g_num_sms / 2 ? p.num_tiles : g_num_sms / 2;
   const cudaError_t e = launch_kernel(zq_gemm2_kernel<BN, KIND>, dim3(2 * pairs), dim3(Cfg::NUM_THREADS),
-                                      Cfg::SMEM_BYTES, st, 1, ta, tb, p);
+                                      Cfg::SMEM_BYTES, st, 1, ta, tb, tc, p);
   if (e != cudaSuccess) {
     set_error("tcgen05 cta-pair gemm launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
@@ -1145,10 +1164,26 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.tma_out = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0) && ((p.ld_out * esz) % 16 == 0) &&
                   (p.row_scales == nullptr || (reinterpret_cast<uintptr_t>(p.row_scales) & 15) == 0) &&
                   (p.bias == nullptr || (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0);
+      CUtensorMap tc;
+      memset(&tc, 0, sizeof(tc));
+      if (p.tma_out) {
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+        cuuint64_t strides[1] = {(cuuint64_t)(p.ld_out * esz)};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t estr[2] = {1, 1};
+        CUtensorMapDataType dt = kind == OUT_S32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                 : kind == OUT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : kind == OUT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        CUresult r = g_encode(&tc, dt, 2, p.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) p.tma_out = 0;
+      }
       p.num_n_tiles = (int)((N + bn2 - 1) / bn2);
       p.num_tiles = (int)mp * p.num_n_tiles;
       p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
-#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, p, st) : launch_gemm2_t<128, KK>(ta, tb, p, st))
+#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, tc, p, st) : launch_gemm2_t<128, KK>(ta, tb, tc, p, st))
       switch (kind) {
         case OUT_S32: return ZQ_G2(OUT_S32);
         case OUT_F32: return ZQ_G2(OUT_F32);
