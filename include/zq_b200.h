@@ -161,6 +161,10 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
                             const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
                             void* stream);
 
+/* Diagnostics / tests: the fp32 GeLU estimate the quantizer brackets with, and
+ * its per-element relative error bound (x clamped to >= -5.5). */
+int zq_gelu_estimate(const float* x, int64_t n, float* est, float* bound, void* stream);
+
 /* Diagnostics: when buf != NULL, subsequent GEMM launches record per-CTA
  * %globaltimer stamps into buf[cta*64 + slot] (slot 0 entry, 1 setup done,
  * 2+4t / 3+4t MMA start / last operands landed for local tile t, 4+4t / 5+4t

@@ -538,6 +538,13 @@ int zq_gelu_quantize(const float* x, int64_t rows, int64_t cols, int64_t ld_x, i
                          flag, as_stream(stream));
 }
 
+int zq_gelu_estimate(const float* x, int64_t n, float* est, float* bound, void* stream) {
+  ZQ_CHECK_ARG(n >= 1, ZQ_ERR_USAGE, "empty input");
+  launch_gelu_estimate(x, n, est, bound, as_stream(stream));
+  ZQ_LAUNCH_CHECK("gelu estimate launch");
+  return ZQ_OK;
+}
+
 int zq_quantize_static(const float* x, int64_t rows, int64_t cols, int64_t ld_x, double scale,
                        int bits, int8_t* q, int64_t ld_q, int32_t* flag, void* stream) {
   ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);

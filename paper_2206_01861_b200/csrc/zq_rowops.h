@@ -12,4 +12,5 @@ int launch_ln_quant_uniform(const float* x, const float* res, const float* gamma
                             int32_t* flag, cudaStream_t st);
 int launch_gelu_quant(const float* x, int64_t rows, int64_t cols, int64_t ld_x, int qm, int8_t* q,
                       int64_t ld_q, float* scales, int32_t* flag, cudaStream_t st);
+void launch_gelu_estimate(const float* x, int64_t n, float* est, float* bound, cudaStream_t st);
 }  // namespace zq

@@ -272,3 +272,24 @@ def test_ln_uniform_and_generic_paths_agree(zq):
         assert same_bits(h(ln), ref), d
         q_ref, s_ref = O.quantize_activation_tokenwise(ref, 8)
         assert same_bits(h(qa.values), q_ref) and same_bits(h(qa.token_scales), s_ref), d
+
+
+def test_gelu_estimate_within_its_bracket(zq):
+    """The bracket the fast GeLU quantizer relies on: |est - gelu_ref| <= bound * |gelu_ref|
+    on a dense grid over [-5.5, 12] (gelu_ref = the exact f32 restatement of
+    tensor.py:76-83, pinned to scipy in tests/test_oracle_golden.py)."""
+    from paper_2206_01861_b200 import _native as N
+
+    x = np.concatenate([np.linspace(-5.5, 12.0, 400_001), np.linspace(-0.01, 0.01, 20_001),
+                        np.linspace(-5.5, -3.0, 50_001)]).astype(F32)
+    xt = torch.from_numpy(x).cuda()
+    est = torch.empty_like(xt)
+    bnd = torch.empty_like(xt)
+    N.call("zq_gelu_estimate", xt.data_ptr(), x.size, est.data_ptr(), bnd.data_ptr(), N.stream_ptr())
+    ref = O.gelu(x).astype(np.float64)
+    e = h(est).astype(np.float64)
+    b = h(bnd).astype(np.float64)
+    nz = ref != 0
+    rel = np.abs(e[nz] - ref[nz]) / np.abs(ref[nz])
+    assert np.all(rel <= b[nz]), (rel.max(), x[nz][np.argmax(rel - b[nz])])
+    assert np.all(e[~nz] == 0.0)
