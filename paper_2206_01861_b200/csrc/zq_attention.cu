@@ -11,20 +11,22 @@
 // "hi" gives the same 3e-6 error as the explicitly truncated value), so the raw
 // TMA-staged tiles serve as hi and only lo is written.
 //
-// One CTA per (sequence, head), seq <= 128, head_dim = 64 (BERT-base, GPT-3
-// 350M heads).  256 threads:
-//   1. one thread TMA-loads Q, K, V of the head (6 boxes of [128 rows x 32 f32],
+// Persistent CTAs (one per SM) walk the (sequence, head) pairs; seq <= 128,
+// head_dim = 64 (BERT-base, GPT-3 350M heads).  256 threads, per head:
+//   1. TMA brings Q, K, V of the head (6 boxes of [128 rows x 32 f32],
 //      SWIZZLE_128B) straight from the fused QKV GEMM output: Q and K land in
 //      the K-major layout the MMA reads;
-//   2. all threads write lo(Q), lo(K) (the same swizzled layout, so a flat
-//      elementwise pass) and transpose V into K-major V^T hi / lo (with B
-//      MN-major the kind::tf32 MMA returned zeros, so only K-major is used);
-//   3. thread 0 issues 24 MMAs for S (M=128, N=128, K=64) -> TMEM cols [0,128);
+//   2. all threads write lo(Q), lo(K) (same swizzled layout, a flat pass) and
+//      transpose V into K-major V^T hi / lo (with B MN-major the kind::tf32 MMA
+//      returned zeros on this build, so only K-major operands are used); the
+//      next head's V load is issued as soon as V is consumed;
+//   3. one warp issues 24 MMAs for S (M=128, N=128, K=64) -> TMEM cols [0,128);
+//      once they complete, Q / K are dead and the next head's Q / K loads go out;
 //   4. 8 warps softmax: warp w reads TMEM lanes 32*(w%4).. (query rows), column
-//      half w/4; row max / sum combined through smem; P hi/lo written to smem
-//      over the (now free) Q/K buffers;
-//   5. thread 0 issues 48 MMAs for O (M=128, N=64, K=128, B = V^T)
-//      -> TMEM cols [128,192);
+//      half w/4; row max / sum combined through smem; P hi / lo are written back
+//      to TMEM (cols [0,128) / [128,256)) with tcgen05.st;
+//   5. one warp issues 48 MMAs for O with A = P read from TMEM, B = V^T
+//      (M=128, N=64, K=128) -> TMEM cols [256,320);
 //   6. 8 warps read O and store ctx rows (f32).
 #include <cuda.h>
 
@@ -40,7 +42,7 @@ constexpr int kAttD = 64;    // head dim
 // of P.V (64 rows = head dim, 4 atoms of 32 tokens).  P hi / lo (128 x 128 f32,
 // 4 K-major atoms each) overlay Qh..Kl once S is computed.
 constexpr int kRegion = kAttT * kAttD * 4;         // 32 KB
-constexpr int kAttSmem = 7 * kRegion + 128 + 2 * 128 * 4;
+constexpr int kAttSmem = 7 * kRegion + 64 + 2 * 128 * 4;
 
 __device__ __forceinline__ uint32_t make_idesc_tf32(int M, int N, int b_mn_major) {
   return (1u << 4)                       // c_format F32
@@ -121,9 +123,40 @@ __device__ __forceinline__ uint32_t sw_off(int rows, int r, int k_bytes) {
   return atom * rows * 128 + r * 128 + ((((wb >> 4) ^ (r & 7))) << 4) + (wb & 15);
 }
 
+__device__ __forceinline__ void mma_tf32_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]),
+      "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),
+      "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Persistent: CTA c handles heads c, c + grid, ...  TMEM (512 columns): S and
+// then P hi in [0,128), P lo in [128,256), O in [256,320).  P never touches smem
+// (the P.V MMAs read A from TMEM), so Q and K are dead as soon as the S MMAs
+// complete and the next head's Q / K TMA loads are issued right then; the next
+// V load goes out as soon as V has been transposed.
 __global__ void __launch_bounds__(256, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tm, int seq, int heads, int dmodel,
-                     int causal, float scale, float* __restrict__ ctx, int64_t ld_ctx, int dbg) {
+                     int causal, float scale, float* __restrict__ ctx, int64_t ld_ctx, int nheads_total) {
   // no static smem in this kernel: the dynamic window starts 1024-aligned, and
   // addressing it directly (no integer round trip) keeps every access LDS/STS
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -134,210 +167,204 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sV = sm + 4 * kRegion;
   uint8_t* sVh = sm + 5 * kRegion;
   uint8_t* sVl = sm + 6 * kRegion;
-  uint8_t* sPh = sQh;  // P (128 x 128 f32 = 64 KB) overlays Q hi/lo
-  uint8_t* sPl = sKh;  // and K hi/lo
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kRegion);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
-  float* red = reinterpret_cast<float*>(bar + 4);  // [2][128] row partials (max / sum)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kRegion);  // QK, V, S, O
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  float* red = reinterpret_cast<float*>(bar + 5);  // [2][128] row partials (max / sum)
 
-  const int b = blockIdx.x / heads, h = blockIdx.x % heads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned long long ts[8];
-  ts[0] = gtime();
-
   if (tid == 0) {
     if (smem_u32(sm) & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
     prefetch_tmap(&tm);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(tslot, 256);
+  if (warp == 0) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  ts[1] = gtime();
-
-  // ---- 1. TMA: Q, K, V boxes of this (sequence, head) ----
-  pdl_trigger();
-  pdl_wait();  // the QKV GEMM output is ready (and the previous ctx reader is done)
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bar[0], 6 * 128 * 128);
-    const int row0 = b * seq;
-#pragma unroll
-    for (int part = 0; part < 3; ++part)
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-        tma_load_2d(sm + (part == 2 ? 4 : 2 * part) * kRegion + j * (kRegion / 2), &tm, &bar[0],
-                    part * dmodel + h * kAttD + 32 * j, row0);
-  }
-  mbar_wait(&bar[0], 0);
-  ts[2] = gtime();
-
-  // ---- 2. split Q, K hi / lo in place (flat pass over the swizzled tiles);
-  //         V -> V^T hi / lo (lane = head-dim column j, 4 consecutive tokens)
-  for (int i = tid; i < 2 * (kRegion / 16); i += 256) {
-    const int part = i / (kRegion / 16), off = (i % (kRegion / 16)) * 16;
-    const float4 x = *reinterpret_cast<const float4*>(sm + 2 * part * kRegion + off);
-    float4 hi, lo;
-    split_tf32(x.x, hi.x, lo.x);
-    split_tf32(x.y, hi.y, lo.y);
-    split_tf32(x.z, hi.z, lo.z);
-    split_tf32(x.w, hi.w, lo.w);
-    *reinterpret_cast<float4*>(sm + (2 * part + 1) * kRegion + off) = lo;
-  }
-  {
-    const int j = (warp & 1) * 32 + lane;  // head-dim column
-    const uint8_t* vcol = sV + (j >> 5) * (kRegion / 2) + (j & 3) * 4;
-    const int jc = (j & 31) >> 2;
-#pragma unroll 2
-    for (int q = warp >> 1; q < kAttT / 4; q += 4) {  // token quad
-      float v[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int t = 4 * q + e;
-        v[e] = *reinterpret_cast<const float*>(vcol + t * 128 + ((jc ^ (t & 7)) << 4));
-      }
-      float4 hi, lo;
-      split_tf32(v[0], hi.x, lo.x);
-      split_tf32(v[1], hi.y, lo.y);
-      split_tf32(v[2], hi.z, lo.z);
-      split_tf32(v[3], hi.w, lo.w);
-      hi = make_float4(v[0], v[1], v[2], v[3]);  // the MMA reads only the tf32 bits
-      const uint32_t o = (q >> 3) * (kAttD * 128) + j * 128 + (((q & 7) ^ (j & 7)) << 4);
-      *reinterpret_cast<float4*>(sVh + o) = hi;
-      *reinterpret_cast<float4*>(sVl + o) = lo;
-    }
-  }
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  ts[3] = gtime();
-  // ---- 3. S = Q K^T (3-term split) ----
-  if (warp == 0) {  // whole warp walks the issue loop (uniform descriptors), one lane issues
-    const uint32_t idesc = make_idesc_tf32(128, 128, 0);
-    const uint64_t dQh = make_sw128_desc(smem_u32(sQh)), dQl = make_sw128_desc(smem_u32(sQl));
-    const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
-#pragma unroll
-    for (int t3 = 0; t3 < 3; ++t3)
-#pragma unroll
-      for (int ks = 0; ks < kAttD / 8; ++ks) {  // K step = 8 tf32 = 32 bytes
-        const int kb = 32 * ks;
-        const uint64_t aoff = (uint64_t)(((kb >> 7) * kAttT * 128 + (kb & 127)) >> 4);
-        mma_tf32_elect(tmem, (t3 == 2 ? dQl : dQh) + aoff, (t3 == 1 ? dKl : dKh) + aoff, idesc,
-                       (t3 | ks) != 0);
-      }
-    mma_commit_elect(&bar[1]);
-  }
-
-  // ---- 4. softmax rows ----
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;  // query index (TMEM lane)
-  mbar_wait(&bar[1], 0);
-  tc_fence_after();
-  ts[4] = gtime();
-  float s[64];
-  {
-    uint32_t r0[32], r1[32];
-    const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + half * 64;
-    tmem_ld_32x32b_x32(ta, r0);
-    tmem_ld_32x32b_x32(ta + 32, r1);
-    tmem_ld_wait();
+
+  auto issue_qk = [&](int hd) {
+    const int b = hd / heads, h = hd % heads;
+    mbar_arrive_expect_tx(&bar[0], 4 * 128 * 128);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      s[j] = __uint_as_float(r0[j]);
-      s[32 + j] = __uint_as_float(r1[j]);
+    for (int part = 0; part < 2; ++part)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        tma_load_2d(sm + 2 * part * kRegion + j * (kRegion / 2), &tm, &bar[0],
+                    part * dmodel + h * kAttD + 32 * j, b * seq);
+  };
+  auto issue_v = [&](int hd) {
+    const int b = hd / heads, h = hd % heads;
+    mbar_arrive_expect_tx(&bar[1], 2 * 128 * 128);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      tma_load_2d(sV + j * (kRegion / 2), &tm, &bar[1], 2 * dmodel + h * kAttD + 32 * j, b * seq);
+  };
+
+  pdl_trigger();
+  pdl_wait();  // the QKV GEMM output is ready (and the previous ctx reader is done)
+  if (tid == 0 && (int)blockIdx.x < nheads_total) {
+    issue_qk(blockIdx.x);
+    issue_v(blockIdx.x);
+  }
+  int it = 0;
+  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+    const uint32_t ph = it & 1;
+    const int nxt = hd + gridDim.x;
+    const int b = hd / heads, h = hd % heads;
+    mbar_wait(&bar[1], ph);
+    mbar_wait(&bar[0], ph);
+    // ---- lo(Q), lo(K) in place; V -> K-major V^T hi / lo ----
+    for (int i = tid; i < 2 * (kRegion / 16); i += 256) {
+      const int part = i / (kRegion / 16), off = (i % (kRegion / 16)) * 16;
+      const float4 x = *reinterpret_cast<const float4*>(sm + 2 * part * kRegion + off);
+      float4 hi, lo;
+      split_tf32(x.x, hi.x, lo.x);
+      split_tf32(x.y, hi.y, lo.y);
+      split_tf32(x.z, hi.z, lo.z);
+      split_tf32(x.w, hi.w, lo.w);
+      *reinterpret_cast<float4*>(sm + (2 * part + 1) * kRegion + off) = lo;
     }
-  }
-  float mx = -INFINITY;
+    {
+      const int j = (warp & 1) * 32 + lane;  // head-dim column
+      const uint8_t* vcol = sV + (j >> 5) * (kRegion / 2) + (j & 3) * 4;
+      const int jc = (j & 31) >> 2;
+#pragma unroll 2
+      for (int q = warp >> 1; q < kAttT / 4; q += 4) {  // token quad
+        float v[4];
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const int key = half * 64 + j;
-    float v = __fmul_rn(s[j], scale);                        // scores *= inv (transformer.py:432)
-    if (key >= seq || (causal && key > row)) v = -INFINITY;  // mask (transformer.py:433-434)
-    s[j] = v;
-    mx = fmaxf(mx, v);
-  }
-  red[half * 128 + row] = mx;
-  __syncthreads();
-  mx = fmaxf(red[row], red[128 + row]);
-  // exp(s - mx) = 2^((s - mx) * log2 e), branch-free: masked scores give 2^-inf = 0
-  // (key 0 is never masked, so mx is finite); relative error ~1e-6
-  float sum = 0.0f;
-#pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const float e = ex2_approx_f(__fmul_rn(__fsub_rn(s[j], mx), 1.4426950408889634f));
-    s[j] = e;
-    sum = __fadd_rn(sum, e);
-  }
-  __syncthreads();
-  red[half * 128 + row] = sum;
-  __syncthreads();
-  sum = __fadd_rn(red[row], red[128 + row]);
-  const float inv_sum = __frcp_rn(sum);
-  // P hi/lo -> smem (rows = queries, K = keys), overlaying Q/K (S MMAs are done)
-#pragma unroll
-  for (int j4 = 0; j4 < 16; ++j4) {
-    float4 ph, pl;
-    float p0 = __fmul_rn(s[4 * j4], inv_sum), p1 = __fmul_rn(s[4 * j4 + 1], inv_sum);
-    float p2 = __fmul_rn(s[4 * j4 + 2], inv_sum), p3 = __fmul_rn(s[4 * j4 + 3], inv_sum);
-    split_tf32(p0, ph.x, pl.x);
-    split_tf32(p1, ph.y, pl.y);
-    split_tf32(p2, ph.z, pl.z);
-    split_tf32(p3, ph.w, pl.w);
-    const uint32_t o = sw_off(kAttT, row, 4 * (half * 64 + 4 * j4));
-    *reinterpret_cast<float4*>(sPh + o) = ph;
-    *reinterpret_cast<float4*>(sPl + o) = pl;
-  }
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  ts[5] = gtime();
-  // ---- 5. O = P V (3-term split), N = 64 ----
-  if (warp == 0) {
-    const uint32_t idesc = make_idesc_tf32(128, kAttD, 0);
-    const uint64_t dPh = make_sw128_desc(smem_u32(sPh)), dPl = make_sw128_desc(smem_u32(sPl));
-    const uint64_t dVh = make_sw128_desc(smem_u32(sVh)), dVl = make_sw128_desc(smem_u32(sVl));
-#pragma unroll
-    for (int t3 = 0; t3 < 3; ++t3)
-#pragma unroll
-      for (int ks = 0; ks < kAttT / 8; ++ks) {
-        const int kb = 32 * ks;
-        const uint64_t aoff = (uint64_t)(((kb >> 7) * kAttT * 128 + (kb & 127)) >> 4);
-        const uint64_t boff = (uint64_t)(((kb >> 7) * kAttD * 128 + (kb & 127)) >> 4);
-        mma_tf32_elect(tmem + 128, (t3 == 2 ? dPl : dPh) + aoff, (t3 == 1 ? dVl : dVh) + boff, idesc,
-                       (t3 | ks) != 0);
+        for (int e = 0; e < 4; ++e) {
+          const int t = 4 * q + e;
+          v[e] = *reinterpret_cast<const float*>(vcol + t * 128 + ((jc ^ (t & 7)) << 4));
+        }
+        float4 hi, lo;
+        split_tf32(v[0], hi.x, lo.x);
+        split_tf32(v[1], hi.y, lo.y);
+        split_tf32(v[2], hi.z, lo.z);
+        split_tf32(v[3], hi.w, lo.w);
+        hi = make_float4(v[0], v[1], v[2], v[3]);  // the MMA reads only the tf32 bits
+        const uint32_t o = (q >> 3) * (kAttD * 128) + j * 128 + (((q & 7) ^ (j & 7)) << 4);
+        *reinterpret_cast<float4*>(sVh + o) = hi;
+        *reinterpret_cast<float4*>(sVl + o) = lo;
       }
-    mma_commit_elect(&bar[2]);
-  }
-  mbar_wait(&bar[2], 0);
-  tc_fence_after();
-  ts[6] = gtime();
-  {
-    uint32_t r0[32];
-    tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16) + 128 + half * 32, r0);
-    tmem_ld_wait();
-    if (row < seq && dbg != 20) {
-      float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(dst + j) =
-            make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
-                        __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
     }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0 && nxt < nheads_total) issue_v(nxt);  // V raw is free again
+
+    // ---- S = Q K^T (3-term split) -> TMEM [0,128) ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_tf32(128, 128, 0);
+      const uint64_t dQh = make_sw128_desc(smem_u32(sQh)), dQl = make_sw128_desc(smem_u32(sQl));
+      const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttD / 8; ++ks) {
+          const int kb = 32 * ks;
+          const uint64_t aoff = (uint64_t)(((kb >> 7) * kAttT * 128 + (kb & 127)) >> 4);
+          mma_tf32_elect(tmem, (t3 == 2 ? dQl : dQh) + aoff, (t3 == 1 ? dKl : dKh) + aoff, idesc,
+                         (t3 | ks) != 0);
+        }
+      mma_commit_elect(&bar[2]);
+    }
+    mbar_wait(&bar[2], ph);
+    tc_fence_after();
+    if (tid == 0 && nxt < nheads_total) issue_qk(nxt);  // Q / K are consumed
+
+    // ---- softmax rows: S from TMEM, P hi / lo back into TMEM ----
+    float s[64];
+    {
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + half * 64;
+      tmem_ld_32x32b_x32(ta, r0);
+      tmem_ld_32x32b_x32(ta + 32, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        s[j] = __uint_as_float(r0[j]);
+        s[32 + j] = __uint_as_float(r1[j]);
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const int key = half * 64 + j;
+      float v = __fmul_rn(s[j], scale);                        // scores *= inv (transformer.py:432)
+      if (key >= seq || (causal && key > row)) v = -INFINITY;  // mask (transformer.py:433-434)
+      s[j] = v;
+      mx = fmaxf(mx, v);
+    }
+    red[half * 128 + row] = mx;
+    __syncthreads();
+    mx = fmaxf(red[row], red[128 + row]);
+    // exp(s - mx) = 2^((s - mx) * log2 e), branch-free: masked scores give 2^-inf = 0
+    float sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const float e = ex2_approx_f(__fmul_rn(__fsub_rn(s[j], mx), 1.4426950408889634f));
+      s[j] = e;
+      sum = __fadd_rn(sum, e);
+    }
+    __syncthreads();
+    red[half * 128 + row] = sum;
+    __syncthreads();
+    sum = __fadd_rn(red[row], red[128 + row]);
+    const float inv_sum = __frcp_rn(sum);
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2) {
+      float hi[32], lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) split_tf32(__fmul_rn(s[32 * c2 + j], inv_sum), hi[j], lo[j]);
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + half * 64 + 32 * c2;
+      tmem_st_32x32b_x32(ta, hi);
+      tmem_st_32x32b_x32(ta + 128, lo);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // ---- O = P V (3-term split), A = P from TMEM, N = 64 -> TMEM [256,320) ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_tf32(128, kAttD, 0);
+      const uint64_t dVh = make_sw128_desc(smem_u32(sVh)), dVl = make_sw128_desc(smem_u32(sVl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttT / 8; ++ks) {
+          const int kb = 32 * ks;
+          const uint64_t boff = (uint64_t)(((kb >> 7) * kAttD * 128 + (kb & 127)) >> 4);
+          mma_tf32_ts_elect(tmem + 256, tmem + (t3 == 2 ? 128 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff,
+                            idesc, (t3 | ks) != 0);
+        }
+      mma_commit_elect(&bar[3]);
+    }
+    mbar_wait(&bar[3], ph);
+    tc_fence_after();
+    {
+      uint32_t r0[32];
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16) + 256 + half * 32, r0);
+      tmem_ld_wait();
+      if (row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
+                          __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM / smem of this head are free for the next one
+    tc_fence_after();
   }
-  tc_fence_before();
-  __syncthreads();
-  ts[7] = gtime();
-  if (dbg == 20 && tid == 0) {
-    unsigned long long* o = reinterpret_cast<unsigned long long*>(ctx) + blockIdx.x * 8;
-    for (int k = 0; k < 8; ++k) o[k] = ts[k];
-  }
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
 int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
@@ -347,10 +374,8 @@ int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols,
 
 using namespace zq;
 
-static int g_att_dbg = 0;
-extern "C" int zq_attention_debug(int mode) {
-  g_att_dbg = mode;
-  return ZQ_OK;
+extern "C" int zq_attention_debug(int mode) {  // phase stamps were removed with the persistent kernel
+  return mode == 0 ? ZQ_OK : ZQ_ERR_UNSUPPORTED;
 }
 
 extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads,
@@ -371,9 +396,17 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     attr = true;
   }
-  const cudaError_t e = launch_kernel(attention_kernel, dim3(batch * heads), dim3(256), kAttSmem,
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int total = batch * heads;
+  const int grid = total < nsm ? total : nsm;
+  const cudaError_t e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem,
                                       reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads,
-                                      heads * head_dim, causal, scale, ctx, ld_ctx, g_att_dbg);
+                                      heads * head_dim, causal, scale, ctx, ld_ctx, total);
   if (e != cudaSuccess) {
     set_error("attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
