@@ -50,15 +50,21 @@ struct GemmParams {
   int debug;                  // diagnostics: 1 = skip global stores, 2 = skip dequant math
 };
 
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
 template <int BN, int W4>
 struct GemmCfg {
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K;
   static constexpr int B_BYTES = BN * BLOCK_K;
   static constexpr int P_BYTES = W4 ? BN * (BLOCK_K / 2) : 0;  // packed INT4 staging
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + P_BYTES;
-  static constexpr int STAGES = 192 * 1024 / STAGE_BYTES > 8 ? 8 : 192 * 1024 / STAGE_BYTES;
-  // per-epilogue-warp output staging: 32 rows x 32 columns x 4 B (f32/s32; f16 uses half)
-  static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 4;
+  // per-epilogue-warp output staging: two 32 rows x 32 columns x 4 B buffers
+  // (bulk TMA stores of one drain while the other is filled)
+  static constexpr int EPI_BYTES = kNumEpiWarps * 2 * 32 * 32 * 4;
+  static constexpr int RING = 232448 - EPI_BYTES - 1024 - 256;
+  static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered int32 accumulators
   static constexpr int NUM_THREADS = (2 + kNumEpiWarps + (W4 ? 4 : 0)) * 32;
   static constexpr int SMEM_BYTES =
@@ -139,29 +145,6 @@ __device__ __forceinline__ void epi_chunk_smem(const uint32_t (&r)[32], float s_
     for (int c = 0; c < 4; ++c)
       *reinterpret_cast<uint4*>(rowp + ((c ^ ((lane >> 1) & 3)) << 4)) =
           make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
-  }
-}
-
-// Coalesced write-back of a staged 32x32 chunk: lane l handles 16-byte piece
-// (l % P) of row (l / P) + step * (32 / P), P = pieces per row (8 for 4-byte,
-// 4 for 2-byte outputs); rows past M are skipped.
-template <int KIND>
-__device__ __forceinline__ void store_chunk_coalesced(const uint8_t* stage, void* out, int64_t ld_out,
-                                                      int row0, int col0, int M, int lane) {
-  constexpr int ESZ = (KIND == OUT_F16 || KIND == OUT_BF16) ? 2 : 4;
-  constexpr int P = 32 * ESZ / 16;   // 16-byte pieces per row
-  constexpr int RPS = 32 / P;        // rows per store instruction
-  const int pc = lane % P, rr = lane / P;
-#pragma unroll
-  for (int st = 0; st < P; ++st) {
-    const int r = st * RPS + rr;
-    const int phys = (ESZ == 4) ? (pc ^ (r & 7)) : (pc ^ ((r >> 1) & 3));
-    const uint4 v = *reinterpret_cast<const uint4*>(stage + r * (32 * ESZ) + phys * 16);
-    if (row0 + r < M) {
-      uint8_t* dst = reinterpret_cast<uint8_t*>(out) +
-                     ((int64_t)(row0 + r) * ld_out + col0) * ESZ + pc * 16;
-      *reinterpret_cast<uint4*>(dst) = v;
-    }
   }
 }
 
@@ -327,7 +310,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
-    uint8_t* stage_c = sC + (warp - 2) * (32 * 32 * 4);
+    uint8_t* stage_c = sC + (warp - 2) * (2 * 32 * 32 * 4);
+    int sbuf = 0;
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
@@ -355,17 +339,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
         }
         const int col0 = n0 + c;
         if (row0 >= p.M || col0 >= p.N) continue;  // warp-uniform
-        if (p.tma_out && col0 + 32 <= p.N) {
-          // stage the 32x32 chunk (row = lane, swizzled) and write it back with
-          // coalesced 16-byte stores: each store instruction covers whole rows
-          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, stage_c, lane);
+        if (p.tma_out) {
+          // double-buffered staging (row = lane, swizzled) drained by bulk TMA
+          // stores that overlap the next chunk's dequant; the map clips M / N
+          uint8_t* sb = stage_c + sbuf * (32 * 32 * 4);
+          if (lane == 0) bulk_wait_read1();
           __syncwarp();
-          if (!(p.debug & 1)) store_chunk_coalesced<KIND>(stage_c, p.out, p.ld_out, row0, col0, p.M, lane);
+          if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, sb, lane);
+          fence_proxy_async_smem();
           __syncwarp();
-        } else if (p.tma_out) {
-          if (row < p.M)
-            epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
-                                 col0, p.N);
+          if (lane == 0 && !(p.debug & 1)) {
+            tma_store_2d(&tmC, sb, col0, row0);
+            bulk_commit();
+          }
+          sbuf ^= 1;
         } else if (row < p.M) {
           epi_chunk_slow<KIND>(r, s_tok, p.row_scales, p.bias, p.out, (int64_t)row * p.ld_out,
                                col0, p.N);
@@ -400,15 +387,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
           uint32_t w[4];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            // SIMD within a register: even / odd nibbles -> bytes, 4-bit sign
+            // extension as b | ((b & 8) * 0x1E) per byte (no cross-byte carries),
+            // then interleave the bytes back into element order with PRMT
             const uint32_t x = h ? pk.y : pk.x;
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              lo |= ((uint32_t)((int32_t)(x << (28 - 4 * e)) >> 28) & 0xFFu) << (8 * e);
-              hi |= ((uint32_t)((int32_t)(x << (12 - 4 * e)) >> 28) & 0xFFu) << (8 * e);
-            }
-            w[2 * h] = lo;
-            w[2 * h + 1] = hi;
+            uint32_t ev = x & 0x0F0F0F0Fu, od = (x >> 4) & 0x0F0F0F0Fu;
+            ev |= (ev & 0x08080808u) * 0x1Eu;
+            od |= (od & 0x08080808u) * 0x1Eu;
+            w[2 * h] = __byte_perm(ev, od, 0x5140);      // elements 0..3
+            w[2 * h + 1] = __byte_perm(ev, od, 0x7362);  // elements 4..7
           }
           *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) * 16)) =
               make_uint4(w[0], w[1], w[2], w[3]);
@@ -456,10 +443,6 @@ struct Gemm2Cfg {
   static constexpr int NUM_THREADS = (2 + kNumEpiWarps) * 32;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
-
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
 
 template <int BN, int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
