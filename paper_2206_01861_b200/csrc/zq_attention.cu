@@ -42,7 +42,7 @@ constexpr int kAttD = 64;    // head dim
 // of P.V (64 rows = head dim, 4 atoms of 32 tokens).  P hi / lo (128 x 128 f32,
 // 4 K-major atoms each) overlay Qh..Kl once S is computed.
 constexpr int kRegion = kAttT * kAttD * 4;         // 32 KB
-constexpr int kAttSmem = 7 * kRegion + 64 + 2 * 128 * 4;
+constexpr int kAttSmem = 7 * kRegion + 64 + 2 * 128 * 4;  // + barriers / TMEM slot / row partials
 
 __device__ __forceinline__ uint32_t make_idesc_tf32(int M, int N, int b_mn_major) {
   return (1u << 4)                       // c_format F32
@@ -367,6 +367,292 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+
+// ---------------------------------------------------------------------------
+// Long sequences (seq > 128, head_dim 64): flash-attention style online softmax
+// over 128-key blocks.  Work item = (sequence, head, 128-query block), heaviest
+// causal blocks first; persistent CTAs.  TMEM: S [0,128), P hi [128,256),
+// P lo [256,384), O [384,448).  Per key block: K (and on the first block Q) land
+// by TMA, lo(K) / V^T are split in smem, S = Q K^T (3xTF32), the row max / sum
+// are carried online (O in TMEM is rescaled by exp(m_old - m_new) before the
+// block's P.V accumulates into it), and the next block's V / K loads are issued
+// as soon as their smem is consumed.  O / l is written at the end.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1)
+    attention_long_kernel(const __grid_constant__ CUtensorMap tm, int seq, int heads, int dmodel,
+                          int causal, float scale, float* __restrict__ ctx, int64_t ld_ctx, int nbh,
+                          int nq) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sQh = sm;
+  uint8_t* sQl = sm + kRegion;
+  uint8_t* sKh = sm + 2 * kRegion;
+  uint8_t* sKl = sm + 3 * kRegion;
+  uint8_t* sV = sm + 4 * kRegion;
+  uint8_t* sVh = sm + 5 * kRegion;
+  uint8_t* sVl = sm + 6 * kRegion;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kRegion);  // Q, K, V, S, O
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+  float* red = reinterpret_cast<float*>(bar + 6);  // [2][128]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nitems = nbh * nq;
+  if (tid == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    prefetch_tmap(&tm);
+    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tPh = tmem + 128, tPl = tmem + 256, tO = tmem + 384;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  uint32_t phQ = 0, phK = 0, phV = 0, phS = 0, phO = 0;
+
+  // item -> (b, h, qb): the heaviest causal query blocks first
+  auto decode = [&](int item, int& b, int& h, int& qb) {
+    qb = nq - 1 - item / nbh;
+    const int bh = item % nbh;
+    b = bh / heads;
+    h = bh % heads;
+  };
+  auto nkeys = [&](int qb) { return causal ? qb + 1 : nq; };
+  auto load_q = [&](int b, int h, int qb) {
+    mbar_arrive_expect_tx(&bar[0], 2 * 128 * 128);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      tma_load_2d(sQh + j * (kRegion / 2), &tm, &bar[0], h * kAttD + 32 * j, b * seq + qb * 128);
+  };
+  auto load_k = [&](int b, int h, int kb) {
+    mbar_arrive_expect_tx(&bar[1], 2 * 128 * 128);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      tma_load_2d(sKh + j * (kRegion / 2), &tm, &bar[1], dmodel + h * kAttD + 32 * j, b * seq + kb * 128);
+  };
+  auto load_v = [&](int b, int h, int kb) {
+    mbar_arrive_expect_tx(&bar[2], 2 * 128 * 128);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      tma_load_2d(sV + j * (kRegion / 2), &tm, &bar[2], 2 * dmodel + h * kAttD + 32 * j, b * seq + kb * 128);
+  };
+
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0 && (int)blockIdx.x < nitems) {
+    int b, h, qb;
+    decode(blockIdx.x, b, h, qb);
+    load_q(b, h, qb);
+    load_k(b, h, 0);
+    load_v(b, h, 0);
+  }
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    int b, h, qb;
+    decode(item, b, h, qb);
+    const int nk = nkeys(qb);
+    const int q0 = qb * 128;
+    int nb = 0, nh = 0, nqb = 0;
+    const int nitem = item + gridDim.x;
+    if (nitem < nitems) decode(nitem, nb, nh, nqb);
+    float m_run = -INFINITY, l_run = 0.0f;
+    for (int kb = 0; kb < nk; ++kb) {
+      const bool last = kb == nk - 1;
+      // ---- lo(K) (and lo(Q) on the first block) while P.V of the previous
+      //      block may still run on the tensor pipe ----
+      if (kb == 0) {
+        mbar_wait(&bar[0], phQ);
+        phQ ^= 1;
+      }
+      mbar_wait(&bar[1], phK);
+      phK ^= 1;
+      for (int i = tid; i < (kb == 0 ? 2 : 1) * (kRegion / 16); i += 256) {
+        const int part = (kb == 0) ? i / (kRegion / 16) : 1;
+        const int off = (i % (kRegion / 16)) * 16;
+        const float4 x = *reinterpret_cast<const float4*>(sm + 2 * part * kRegion + off);
+        float4 hi, lo;
+        split_tf32(x.x, hi.x, lo.x);
+        split_tf32(x.y, hi.y, lo.y);
+        split_tf32(x.z, hi.z, lo.z);
+        split_tf32(x.w, hi.w, lo.w);
+        *reinterpret_cast<float4*>(sm + (2 * part + 1) * kRegion + off) = lo;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      // ---- S = Q K^T (queued behind the previous P.V) ----
+      if (warp == 0) {
+        const uint32_t idesc = make_idesc_tf32(128, 128, 0);
+        const uint64_t dQh = make_sw128_desc(smem_u32(sQh)), dQl = make_sw128_desc(smem_u32(sQl));
+        const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttD / 8; ++ks) {
+            const int kbt = 32 * ks;
+            const uint64_t aoff = (uint64_t)(((kbt >> 7) * kAttT * 128 + (kbt & 127)) >> 4);
+            mma_tf32_elect(tS, (t3 == 2 ? dQl : dQh) + aoff, (t3 == 1 ? dKl : dKh) + aoff, idesc,
+                           (t3 | ks) != 0);
+          }
+        mma_commit_elect(&bar[3]);
+      }
+      // ---- V^T of this block once the previous P.V no longer reads it ----
+      if (kb > 0) {
+        mbar_wait(&bar[4], phO);
+        phO ^= 1;
+        tc_fence_after();
+      }
+      mbar_wait(&bar[2], phV);
+      phV ^= 1;
+      {
+        const int j = (warp & 1) * 32 + lane;
+        const uint8_t* vcol = sV + (j >> 5) * (kRegion / 2) + (j & 3) * 4;
+        const int jc = (j & 31) >> 2;
+#pragma unroll 2
+        for (int q = warp >> 1; q < kAttT / 4; q += 4) {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int t = 4 * q + e;
+            v[e] = *reinterpret_cast<const float*>(vcol + t * 128 + ((jc ^ (t & 7)) << 4));
+          }
+          float4 hi, lo;
+          split_tf32(v[0], hi.x, lo.x);
+          split_tf32(v[1], hi.y, lo.y);
+          split_tf32(v[2], hi.z, lo.z);
+          split_tf32(v[3], hi.w, lo.w);
+          hi = make_float4(v[0], v[1], v[2], v[3]);
+          const uint32_t o = (q >> 3) * (kAttD * 128) + j * 128 + (((q & 7) ^ (j & 7)) << 4);
+          *reinterpret_cast<float4*>(sVh + o) = hi;
+          *reinterpret_cast<float4*>(sVl + o) = lo;
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (tid == 0) {  // V raw is consumed: next block's (or next item's first) V
+        if (!last) load_v(b, h, kb + 1);
+        else if (nitem < nitems) load_v(nb, nh, 0);
+      }
+      mbar_wait(&bar[3], phS);
+      phS ^= 1;
+      tc_fence_after();
+      if (tid == 0) {  // K (and after the last block, Q) are consumed
+        if (!last) {
+          load_k(b, h, kb + 1);
+        } else if (nitem < nitems) {
+          load_q(nb, nh, nqb);
+          load_k(nb, nh, 0);
+        }
+      }
+      // ---- online softmax ----
+      float sv[64];
+      {
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tS + ((uint32_t)(quarter * 32) << 16) + half * 64;
+        tmem_ld_32x32b_x32(ta, r0);
+        tmem_ld_32x32b_x32(ta + 32, r1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sv[j] = __uint_as_float(r0[j]);
+          sv[32 + j] = __uint_as_float(r1[j]);
+        }
+      }
+      float mx = -INFINITY;
+      const int qrow = q0 + row;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = kb * 128 + half * 64 + j;
+        float v = __fmul_rn(sv[j], scale);
+        if (key >= seq || (causal && key > qrow)) v = -INFINITY;
+        sv[j] = v;
+        mx = fmaxf(mx, v);
+      }
+      red[half * 128 + row] = mx;
+      __syncthreads();
+      const float m_new = fmaxf(m_run, fmaxf(red[row], red[128 + row]));
+      const float m_use = m_new == -INFINITY ? 0.0f : m_new;  // fully masked so far
+      const float corr = ex2_approx_f(__fmul_rn(__fsub_rn(m_run, m_use), 1.4426950408889634f));
+      float sum = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const float e = ex2_approx_f(__fmul_rn(__fsub_rn(sv[j], m_use), 1.4426950408889634f));
+        sv[j] = e;
+        sum = __fadd_rn(sum, e);
+      }
+      __syncthreads();
+      red[half * 128 + row] = sum;
+      __syncthreads();
+      l_run = __fadd_rn(__fmul_rn(l_run, corr), __fadd_rn(red[row], red[128 + row]));
+      m_run = m_new;
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        float hi[32], lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) split_tf32(sv[32 * c2 + j], hi[j], lo[j]);
+        const uint32_t ta = ((uint32_t)(quarter * 32) << 16) + half * 64 + 32 * c2;
+        tmem_st_32x32b_x32(tPh + ta, hi);
+        tmem_st_32x32b_x32(tPl + ta, lo);
+      }
+      if (kb > 0) {  // rescale the running O (this warp's 32 columns)
+        uint32_t r0[32];
+        const uint32_t ta = tO + ((uint32_t)(quarter * 32) << 16) + half * 32;
+        tmem_ld_32x32b_x32(ta, r0);
+        tmem_ld_wait();
+        float o[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = __fmul_rn(__uint_as_float(r0[j]), corr);
+        tmem_st_32x32b_x32(ta, o);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      // ---- O += P V ----
+      if (warp == 0) {
+        const uint32_t idesc = make_idesc_tf32(128, kAttD, 0);
+        const uint64_t dVh = make_sw128_desc(smem_u32(sVh)), dVl = make_sw128_desc(smem_u32(sVl));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttT / 8; ++ks) {
+            const int kbt = 32 * ks;
+            const uint64_t boff = (uint64_t)(((kbt >> 7) * kAttD * 128 + (kbt & 127)) >> 4);
+            mma_tf32_ts_elect(tO, (t3 == 2 ? tPl : tPh) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                              (kb | t3 | ks) != 0);
+          }
+        mma_commit_elect(&bar[4]);
+      }
+    }
+    // ---- epilogue: ctx = O / l ----
+    mbar_wait(&bar[4], phO);
+    phO ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r0[32];
+      tmem_ld_32x32b_x32(tO + ((uint32_t)(quarter * 32) << 16) + half * 32, r0);
+      tmem_ld_wait();
+      const float inv_l = __frcp_rn(l_run);
+      if (q0 + row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + q0 + row) * ld_ctx + h * kAttD + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(
+              __fmul_rn(__uint_as_float(r0[j]), inv_l), __fmul_rn(__uint_as_float(r0[j + 1]), inv_l),
+              __fmul_rn(__uint_as_float(r0[j + 2]), inv_l), __fmul_rn(__uint_as_float(r0[j + 3]), inv_l));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
                   int box_cols, int box_rows, CUtensorMapSwizzle sw);
 
@@ -382,8 +668,7 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
                                 int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
                                 void* stream) {
   ZQ_CHECK_ARG(batch >= 1 && seq >= 1 && heads >= 1, ZQ_ERR_SHAPE, "bad attention shape");
-  ZQ_CHECK_ARG(seq <= kAttT && head_dim == kAttD, ZQ_ERR_UNSUPPORTED,
-               "fused attention supports seq <= 128 and head_dim == 64");
+  ZQ_CHECK_ARG(head_dim == kAttD, ZQ_ERR_UNSUPPORTED, "fused attention supports head_dim == 64");
   ZQ_CHECK_ARG(ld_qkv % 4 == 0 && ld_ctx % 4 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                ZQ_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
@@ -394,6 +679,7 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
+    cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     attr = true;
   }
   int nsm = 148;
@@ -403,10 +689,19 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int total = batch * heads;
-  const int grid = total < nsm ? total : nsm;
-  const cudaError_t e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem,
-                                      reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads,
-                                      heads * head_dim, causal, scale, ctx, ld_ctx, total);
+  cudaError_t e;
+  if (seq <= kAttT) {
+    const int grid = total < nsm ? total : nsm;
+    e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem, reinterpret_cast<cudaStream_t>(stream),
+                      1, tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, total);
+  } else {
+    const int nq = (seq + kAttT - 1) / kAttT;
+    const int items = total * nq;
+    const int grid = items < nsm ? items : nsm;
+    e = launch_kernel(attention_long_kernel, dim3(grid), dim3(256), kAttSmem,
+                      reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads, heads * head_dim, causal,
+                      scale, ctx, ld_ctx, total, nq);
+  }
   if (e != cudaSuccess) {
     set_error("attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;

@@ -223,7 +223,7 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
   // at most 8 (portable cluster), keeping >= 32 keys per chunk
   int C = 1;
   while (C < 8 && (int64_t)batch * heads * C < 4 * 148 && max_ctx / (2 * C) >= 32) C *= 2;
-  const int chunk = (int)((max_ctx + C - 1) / C);
+  const int chunk = (int)(((max_ctx + C - 1) / C + 3) / 4 * 4);  // keeps the partial-output rows 16-byte aligned
   const int G = kDecThreads / (head_dim / 4);
   const size_t smem = sizeof(float) * (256 + (size_t)chunk + (size_t)G * head_dim);
   ZQ_CHECK_ARG(smem <= 200 * 1024, ZQ_ERR_UNSUPPORTED, "context too long for decode attention");

@@ -270,13 +270,13 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int,
 
     q, k, v are column views of one [T, 3d] qkv buffer (as produced by the fused
     QKV GEMM): then the fused tcgen05 kernel (zq_attention_f32, 3xTF32 split,
-    ~fp32 accuracy) runs for t <= 128, head_dim 64; other shapes use torch's
+    ~fp32 accuracy; online softmax over 128-key blocks for t > 128) runs for head_dim 64; other head sizes use torch's
     float32 scaled-dot-product attention."""
     bt, d = q.shape
     t = bt // batch
     dh = d // num_heads
     scale = float(np.float32(1.0 / math.sqrt(dh)))
-    fused = (t <= 128 and dh == 64 and q.stride(1) == 1 and k.data_ptr() == q.data_ptr() + 4 * d
+    fused = (dh == 64 and q.stride(1) == 1 and k.data_ptr() == q.data_ptr() + 4 * d
              and v.data_ptr() == q.data_ptr() + 8 * d and q.stride(0) == k.stride(0) == v.stride(0))
     if fused:
         ctx = out if out is not None else torch.empty((bt, d), dtype=torch.float32, device=q.device)

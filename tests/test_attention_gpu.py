@@ -20,12 +20,12 @@ def ref_attention(qkv, batch, seq, heads, dh, causal):
     return (p @ v).transpose(1, 2).reshape(batch * seq, d)
 
 
-@pytest.mark.parametrize("seq", [128, 77, 1, 16])
+@pytest.mark.parametrize("seq", [128, 77, 1, 16, 129, 300, 1024])
 @pytest.mark.parametrize("causal", [False, True])
 def test_fused_attention_close_to_f64(seq, causal):
     from paper_2206_01861_b200 import transformer as T
 
-    batch, heads, dh = 3, 12, 64
+    batch, heads, dh = (3, 12, 64) if seq <= 128 else (2, 4, 64)
     d = heads * dh
     torch.manual_seed(seq + causal)
     qkv = torch.randn(batch * seq, 3 * d, device="cuda") * 1.5
@@ -33,4 +33,7 @@ def test_fused_attention_close_to_f64(seq, causal):
     ref = ref_attention(qkv, batch, seq, heads, dh, causal)
     err = (out.double() - ref).abs().max().item()
     rel = ((out.double() - ref).norm() / ref.norm()).item()
-    assert rel < 1e-5 and err < 1e-4, (rel, err)  # fp32-level (tf32 alone would be ~1e-3)
+    # fp32-level (tf32 alone would be ~1e-3); the online softmax over many key
+    # blocks (seq > 128) adds one rescale rounding per block
+    tol = 1e-5 if seq <= 128 else 3e-5
+    assert rel < tol and err < 1e-4, (rel, err)

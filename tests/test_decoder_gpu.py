@@ -82,13 +82,13 @@ def test_decode_attention_vs_torch():
     from paper_2206_01861_b200 import _native as N
 
     for dh, heads in ((64, 4), (96, 3), (256, 2)):
-        batch, max_ctx = 3, 40
+        batch, max_ctx = 3, 1041  # odd context: chunked over a cluster
         dl = dh * heads
         torch.manual_seed(dh)
         kc = torch.randn(batch, max_ctx, dl, device="cuda")
         vc = torch.randn(batch, max_ctx, dl, device="cuda")
         q = torch.randn(batch, 3 * dl, device="cuda")
-        lens = torch.tensor([1, 17, 40], dtype=torch.int32, device="cuda")
+        lens = torch.tensor([1, 517, 1041], dtype=torch.int32, device="cuda")
         ctx = torch.empty(batch, dl, device="cuda")
         scale = 1.0 / dh ** 0.5
         N.call("zq_decode_attention_f32", q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), max_ctx,

@@ -29,3 +29,23 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def long_seq():
+    """GPT-3 350M prefill attention: batch 8, seq 1024, 16 heads x 64, causal."""
+    batch, seq, heads, dh = 8, 1024, 16, 64
+    d = heads * dh
+    t = batch * seq
+    q = torch.randn(t, 3 * d, device="cuda")
+    c = torch.empty(t, d, device="cuda")
+    sec = graph_time([lambda: T.attention(q[:, :d], q[:, d:2 * d], q[:, 2 * d:], heads, True, batch, out=c)])
+    import torch.nn.functional as F
+    hq = lambda z: z.reshape(batch, seq, heads, dh).transpose(1, 2)  # noqa: E731
+    sec2 = graph_time([lambda: F.scaled_dot_product_attention(hq(q[:, :d]), hq(q[:, d:2 * d]), hq(q[:, 2 * d:]),
+                                                              is_causal=True)])
+    print(json.dumps({"kernel": "attention_long", "seq": seq, "us": round(sec * 1e6, 1),
+                      "torch_sdpa_f32_us": round(sec2 * 1e6, 1)}))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "long":
+    long_seq()
