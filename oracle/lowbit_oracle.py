@@ -425,6 +425,30 @@ def block_forward(x, qb: dict, num_heads: int, causal: bool, act_mode: str = "in
     return layer_norm_numpy(h + f, qb["ln2_gamma"], qb["ln2_beta"], LN_EPS)
 
 
+def block_forward_static(x, qb: dict, num_heads: int, causal: bool, layer: int,
+                         static_scales: dict) -> np.ndarray:
+    """pkg/src/lowbit/transformer.py:443-486 with activation_static=True: every
+    GEMM-input site quantizes with its calibrated scale (_act_mode_for,
+    transformer.py:386-402 -> StaticAct; igemm.py:131-134)."""
+    x = np.ascontiguousarray(x, dtype=F32)
+
+    def lin(inp, name, bname, site):
+        vals, rs, bits = qb[name]
+        return quantized_linear(inp, vals, rs, qb[bname], "static",
+                                static_scale=static_scales[f"layer{layer}.{site}"], w_bits=bits)
+
+    q = lin(x, "w_q", "b_q", "attn_in")
+    k = lin(x, "w_k", "b_k", "attn_in")
+    v = lin(x, "w_v", "b_v", "attn_in")
+    ctx = attention(q, k, v, num_heads, causal)
+    attn_out = lin(ctx, "w_o", "b_o", "attn_proj_in")
+    h = layer_norm_numpy(x + attn_out, qb["ln1_gamma"], qb["ln1_beta"], LN_EPS)
+    u = lin(h, "w_h4h", "b_h4h", "ffc_in")
+    z = gelu(u)
+    f = lin(z, "w_4hh", "b_4hh", "ffc_mid")
+    return layer_norm_numpy(h + f, qb["ln2_gamma"], qb["ln2_beta"], LN_EPS)
+
+
 # ---------------------------------------------------------------------------
 # Deterministic synthetic inputs: pkg/src/lowbit/tensor.py:113-164
 # ---------------------------------------------------------------------------

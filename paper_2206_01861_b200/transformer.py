@@ -344,6 +344,63 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
     return y
 
 
+def float_block_forward(x: torch.Tensor, w: dict, num_heads: int, causal: bool, layer: int = 0,
+                        tap=None) -> torch.Tensor:
+    """transformer.py:443-486 with float weights (PrecisionConfig.full()): the
+    calibration forward.  `w` holds float32 device tensors (w_q .. ln2_beta);
+    `tap(site, layer, x)` sees the float tensor entering each weight GEMM."""
+    def lin(inp, wn, bn):
+        return torch.addmm(w[bn], inp, w[wn].t())
+
+    if tap is not None:
+        tap("attn_in", layer, x)
+    q, k, v = lin(x, "w_q", "b_q"), lin(x, "w_k", "b_k"), lin(x, "w_v", "b_v")
+    t, d = x.shape
+    dh = d // num_heads
+    heads = lambda z: z.reshape(1, t, num_heads, dh).transpose(1, 2)  # noqa: E731
+    ctx = torch.nn.functional.scaled_dot_product_attention(
+        heads(q), heads(k), heads(v), is_causal=causal,
+        scale=float(np.float32(1.0 / math.sqrt(dh)))).transpose(1, 2).reshape(t, d)
+    if tap is not None:
+        tap("attn_proj_in", layer, ctx)
+    h = torch.nn.functional.layer_norm(x + lin(ctx, "w_o", "b_o"), (d,), w["ln1_gamma"], w["ln1_beta"], LN_EPS)
+    if tap is not None:
+        tap("ffc_in", layer, h)
+    z = torch.nn.functional.gelu(lin(h, "w_h4h", "b_h4h"))
+    if tap is not None:
+        tap("ffc_mid", layer, z)
+    f = lin(z, "w_4hh", "b_4hh")
+    return torch.nn.functional.layer_norm(h + f, (d,), w["ln2_gamma"], w["ln2_beta"], LN_EPS)
+
+
+def calibrate_static_scales(float_blocks: list[dict], batches, num_heads: int, causal: bool,
+                            momentum: float = 0.95, bits: int = 8) -> dict[str, float]:
+    """evaluate.calibrate_model (evaluate.py:168-200) on device: every calibration
+    batch (float32 [tokens, d] block-0 inputs) runs through the float blocks with
+    one `quant.Calibrator` per GEMM-input site "layer{L}.{site}" (momentum
+    min/max, quant.py:289-330, extrema reduced on device); returns the finalized
+    static scales for `block_forward(..., static_scales=...)` under a
+    `PrecisionConfig(..., activation_static=True)`."""
+    cals: dict[str, quant.Calibrator] = {}
+
+    def tap(site, layer, x):
+        key = f"layer{layer}.{site}"
+        if key not in cals:
+            cals[key] = quant.Calibrator(momentum=momentum)
+        cals[key].observe(x)
+
+    dev_blocks = [{k: as_device_f32(v) for k, v in b.items() if k != "num_heads"} for b in float_blocks]
+    n = 0
+    for xb in batches:
+        x = as_device_f32(xb)
+        for li, w in enumerate(dev_blocks):
+            x = float_block_forward(x, w, num_heads, causal, li, tap)
+        n += 1
+    if n == 0:
+        raise UsageError("calibration needs at least one batch")
+    return {k: c.finalize(bits) for k, c in sorted(cals.items())}
+
+
 # ---------------------------------------------------------------------------
 # Batched encoder / decoder-prefill engine (the benchmark caller)
 # ---------------------------------------------------------------------------

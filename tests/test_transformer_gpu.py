@@ -105,3 +105,63 @@ def test_encoder_engine_matches_block_forward():
     # graph replay is deterministic
     out2 = eng.forward(ids).clone()
     assert torch.equal(out, out2)
+
+
+def _float_weights(rng, d, f):
+    w = {n: rng.gaussian(s, std=0.05) for n, s in (
+        ("w_q", (d, d)), ("w_k", (d, d)), ("w_v", (d, d)), ("w_o", (d, d)),
+        ("w_h4h", (f, d)), ("w_4hh", (d, f)))}
+    for n, s in (("b_q", d), ("b_k", d), ("b_v", d), ("b_o", d), ("b_h4h", f), ("b_4hh", d)):
+        w[n] = rng.gaussian((s,), std=0.02)
+    for n in ("ln1", "ln2"):
+        w[f"{n}_gamma"] = (1.0 + rng.gaussian((d,), std=0.1)).astype(F32)
+        w[f"{n}_beta"] = rng.gaussian((d,), std=0.1)
+    return w
+
+
+def _oracle_float_block(x, w, heads, causal, layer, tap):
+    """transformer.py:443-486 with float weights (the calibration forward)."""
+    lin = lambda inp, a, b: O.matmul_f32(inp, w[a].T) + w[b]  # noqa: E731
+    tap("attn_in", layer, x)
+    ctx = O.attention(lin(x, "w_q", "b_q"), lin(x, "w_k", "b_k"), lin(x, "w_v", "b_v"), heads, causal)
+    tap("attn_proj_in", layer, ctx)
+    h = O.layer_norm_numpy(x + lin(ctx, "w_o", "b_o"), w["ln1_gamma"], w["ln1_beta"])
+    tap("ffc_in", layer, h)
+    z = O.gelu(lin(h, "w_h4h", "b_h4h"))
+    tap("ffc_mid", layer, z)
+    return O.layer_norm_numpy(h + lin(z, "w_4hh", "b_4hh"), w["ln2_gamma"], w["ln2_beta"])
+
+
+def test_static_calibration_and_static_forward():
+    """§8f row 3: calibration on device (evaluate.py:168-200 over the float blocks,
+    one momentum Calibrator per GEMM-input site) reproduces the reference's
+    calibrated scales, and the static-activation block forward (StaticAct at every
+    site, transformer.py:386-402) matches the reference block with those scales."""
+    from paper_2206_01861_b200 import transformer as T
+
+    d, heads, f, L = 128, 4, 512, 2
+    rng = O.Rng(11)
+    ws = [_float_weights(rng, d, f) for _ in range(L)]
+    batches = [rng.gaussian((48, d), std=0.5) for _ in range(3)]
+    scales = T.calibrate_static_scales(ws, batches, heads, causal=True)
+    cals = {}
+
+    def tap(site, layer, x):
+        cals.setdefault(f"layer{layer}.{site}", O.Calibrator()).observe(x)
+
+    for xb in batches:
+        x = xb
+        for li, w in enumerate(ws):
+            x = _oracle_float_block(x, w, heads, True, li, tap)
+    ref_scales = {k: c.finalize(8) for k, c in cals.items()}
+    assert sorted(scales) == sorted(ref_scales)
+    for k in ref_scales:  # float forwards differ in rounding only
+        assert abs(scales[k] - ref_scales[k]) <= 1e-4 * ref_scales[k], k
+    prec = T.PrecisionConfig.from_scheme("W8A8", group_count=16, activation_static=True)
+    x = batches[0]
+    for li, w in enumerate(ws):
+        db = T.quantize_block(dict(w, num_heads=heads), prec)
+        y = T.block_forward(x, db, prec, True, layer=li, static_scales=ref_scales).cpu().numpy()
+        ref = O.block_forward_static(x, O.quantize_block(w, 8, 8, 16), heads, True, li, ref_scales)
+        assert rel(y, ref) < TOL, (li, rel(y, ref))
+        x = ref
