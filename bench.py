@@ -563,12 +563,20 @@ def run_c1(args, rank: int, world: int, dist):
         step(sets[i % 8])
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
+    # one CUDA graph per rotating input (the two launches of a step, no host gaps)
+    graphs = []
+    for i in range(8):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step(sets[i])
+        graphs.append(g)
+    torch.cuda.synchronize()
     ev = []
     with ClockSampler(torch.cuda.current_device()) as clk:
         for i in range(args.steps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            step(sets[i % 8])
+            graphs[i % 8].replay()
             b.record(stream)
             ev.append((a, b))
         torch.cuda.synchronize()

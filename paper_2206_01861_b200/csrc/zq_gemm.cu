@@ -439,7 +439,8 @@ struct Gemm2Cfg {
   static constexpr int EPI_BYTES = kNumEpiWarps * 2 * 32 * 32 * 4;
   static constexpr int RING = 232448 - EPI_BYTES - 1024 - 256;
   static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;
+  // double-buffered accumulators: 2*BN columns, allocated as a power of two (BN = 192 -> 512)
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static constexpr int NUM_THREADS = (2 + kNumEpiWarps) * 32;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
@@ -1117,8 +1118,8 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       // stores at ~35 GB/s/SM); rounds = ceil(tiles / pairs)
       const int esz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : (kind == OUT_S32 ? 4 : 4);
       double best = 1e30;
-      for (int cand = 256; cand >= 128; cand -= 128) {
-        if (cand == 256 && N < 256) continue;
+      for (int cand : {256, 192, 128}) {
+        if (cand > N && cand > 128) continue;
         const double tiles = (double)mp * (double)((N + cand - 1) / cand);
         const double rounds = std::ceil(tiles / (g_num_sms / 2));
         const double t_mma = 128.0 * cand * K / 11.1e12;
@@ -1166,7 +1167,9 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.num_n_tiles = (int)((N + bn2 - 1) / bn2);
       p.num_tiles = (int)mp * p.num_n_tiles;
       p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
-#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, tc, p, st) : launch_gemm2_t<128, KK>(ta, tb, tc, p, st))
+#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, tc, p, st) \
+                   : bn2 == 192 ? launch_gemm2_t<192, KK>(ta, tb, tc, p, st)  \
+                                : launch_gemm2_t<128, KK>(ta, tb, tc, p, st))
       switch (kind) {
         case OUT_S32: return ZQ_G2(OUT_S32);
         case OUT_F32: return ZQ_G2(OUT_F32);
