@@ -238,8 +238,25 @@ def gemm_roofline(torch, eng, peaks, basis):
             events.append((a, b, 2 * m * k * n, nbytes))
         return timed_linear
 
-    for e, o in zip(engines, origs):
+    origs_ln = [e._linear_ln for e in engines]
+
+    def make_timed_ln(orig):
+        def timed(q, s, w, bias, res, g, b, ln_out, qo, so, ws):
+            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ok = orig(q, s, w, bias, res, g, b, ln_out, qo, so, ws)
+            b2.record()
+            if ok:  # GEMM + residual read + LN out f32 + int8 + scales
+                m, k = q.shape
+                n = w.rows
+                nbytes = m * k + n * k + 4 * m * n + 4 * m * n + m * n + 8 * m + 16 * n
+                events.append((a, b2, 2 * m * k * n, nbytes))
+            return ok
+        return timed
+
+    for e, o, ol in zip(engines, origs, origs_ln):
         e._linear = make_timed(o)
+        e._linear_ln = make_timed_ln(ol)
     try:
         for _ in range(3):
             events.clear()
@@ -247,8 +264,9 @@ def gemm_roofline(torch, eng, peaks, basis):
                 e._run()
         torch.cuda.synchronize()
     finally:
-        for e, o in zip(engines, origs):
+        for e, o, ol in zip(engines, origs, origs_ln):
             e._linear = o
+            e._linear_ln = ol
     times = [a.elapsed_time(b) * 1e-3 for a, b, _, _ in events]
     t = sum(times)
     ops = sum(o for _, _, o, _ in events)
@@ -264,7 +282,8 @@ def gemm_roofline(torch, eng, peaks, basis):
     achieved = nbytes / t / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-            "kernel": "zq_gemm2_kernel (fused W8A8 linear, tcgen05 kind::i8 CTA pairs)",
+            "kernel": "zq_gemm2_kernel / zq_gemm2_ln_kernel (W8A8 linear, tcgen05 kind::i8 CTA pairs; the O and "
+                      "4hh projections with residual + LayerNorm + quantize fused in)",
             "launches_per_step": len(events), "per_launch_us": 1e6 * t / max(1, len(events)),
             "algorithmic_bytes_per_launch": nbytes / max(1, len(events)),
             "tensor_tflops": ops / t / 1e12, "tensor_peak": p_int8 / 1e12,
@@ -339,7 +358,8 @@ def run_ours(args, rank: int, world: int, dist):
         return
     cores = len(os.sched_getaffinity(0))
     cpu_val, cpu_sample, _ = cpu_reference_sample(cores, 1)
-    launches_per_step = 2 + 9 * BERT["layers"]  # tok quant + 9 per block + final LN
+    fused = all(e._fuse_ln for e in (eng._sub or [eng]))
+    launches_per_step = 2 + (7 if fused else 9) * BERT["layers"]  # tok quant + per block + final LN
     line = {
         "metric": "BERT-base W8A8 encoder forward throughput", "value": value, "unit": "seq/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -110,6 +110,22 @@ int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float s
               const float* bias, int64_t M, int64_t N, int64_t K, void* out, int64_t ld_out,
               int out_type, void* stream);
 
+/* Fused row-parallel projection + residual + LayerNorm + token-wise quantize
+ * (transformer.py:474-477 and :484-486 as one kernel): y = LN(residual + linear)
+ * with the exact epilogue of zq_linear, numpy's pairwise LN of
+ * zq_layer_norm_quantize, and its token-wise quantization; writes y (f32) and
+ * q / q_scales, never the linear output.  Needs w_bits 8 and a row width whose
+ * pairwise tree is balanced with 96- or 128-element leaves (768, 1024, 2048,
+ * 3072, 4096, 6144, ...); returns ZQ_ERR_UNSUPPORTED otherwise (callers then
+ * run zq_linear + zq_layer_norm_quantize).  `workspace`: device memory of at
+ * least 4*ceil(M/256) + 16 + 12*M*(N/(2*leaf)) bytes, zero-initialised once and
+ * then reused by every call with the same N on the same stream. */
+int zq_linear_ln_quantize(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq,
+                          int64_t ld_w, int w_bits, const float* w_row_scales, const float* bias, int64_t M,
+                          int64_t N, int64_t K, const float* residual, const float* gamma, const float* beta,
+                          float eps, int bits, float* ln_out, int8_t* q, int64_t ld_q, float* q_scales,
+                          void* workspace, int64_t workspace_bytes, int32_t* nonfinite_flag, void* stream);
+
 /* Standalone dequant epilogue over an int32 accumulator (igemm.py:83-112); used
  * after the tensor-parallel int32 all-reduce. */
 int zq_dequant_epilogue(const int32_t* acc, int64_t ld_acc, const float* token_scales,

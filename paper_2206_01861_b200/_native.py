@@ -35,6 +35,8 @@ _SIGS = {
     "zq_gelu_quantize": [_p, _i64, _i64, _i64, _i32, _p, _p, _i64, _p, _p, _p],
     "zq_igemm_s32": [_p, _i64, _p, _i64, _i32, _i64, _i64, _i64, _p, _i64, _p],
     "zq_linear": [_p, _i64, _p, _f32, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p],
+    "zq_linear_ln_quantize": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _p, _p, _f32, _i32, _p,
+                              _p, _i64, _p, _p, _i64, _p, _p],
     "zq_dequant_epilogue": [_p, _i64, _p, _f32, _p, _p, _i64, _i64, _p, _i64, _i32, _p],
     "zq_linear_full": [_p, _i64, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p],
     "zq_row_absmax": [_p, _i64, _i64, _i64, _p, _p, _p],

@@ -806,6 +806,391 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) tmem_dealloc(tmem, MP < 32 ? 32 : MP);
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused row-parallel projection + residual + LayerNorm + token-wise quantize
+// (transformer.py:474-477 / :484-486: y = LN(x + linear(q, w)), igemm.py:150-157):
+//   f  = ((f32(acc) * s_tok) * s_w) + bias      (igemm.py:107-111, exact order)
+//   v  = x + f                                   (residual, f32)
+//   y  = LN(v) with numpy's pairwise mean / variance (tensor.py:59-73)
+//   q, s = token-wise quantize(y)                (quant.py:258-269)
+// The GEMM's output never goes to HBM: only y (f32, the next residual) and q /
+// scales are written.  A pair tile is 256 rows x BN columns and BN / 2 = L is
+// exactly one leaf of numpy's pairwise tree for the row width N = NT * BN
+// (N = L * 2^k), so each epilogue thread owns one leaf of one row in registers
+// and evaluates it with numpy's 8-chain leaf order.  The tree above the leaves
+// spans the NT tiles of a row block; their partial sums / maxima are exchanged
+// through global memory with a release/acquire counter per row block (three
+// rounds: sum, squared deviations, max).  All tiles of a row block are in the
+// same round of the persistent grid (tiles_per_round = floor(pairs / NT) * NT)
+// and every CTA is co-resident, so the exchange cannot deadlock.  The counter is
+// never reset: each launch adds exactly 6 * NT per row block, so a CTA derives
+// this launch's base from the value its first increment returns.
+// ---------------------------------------------------------------------------
+struct LnFuseParams {
+  const float* residual;  // [M, N] f32 (x)
+  const float* gamma;
+  const float* beta;
+  float eps;
+  float* ln_out;          // [M, N] f32 (y)
+  int8_t* q;              // [M, ld_q]
+  int64_t ld_q;
+  float* q_scales;        // [M]
+  int qm;
+  float* partials;        // [3][M][NT]
+  unsigned int* counters; // [ceil(M / 256)], zero at allocation, never reset
+  int32_t* flag;
+  int tiles_per_round;
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps (256 threads)
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+template <int L>
+__device__ __forceinline__ float leaf_sum(const float (&v)[L]) {  // numpy pairwise leaf (L <= 128)
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = v[j];
+#pragma unroll
+  for (int i = 8; i < L; i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], v[i + j]);
+  return __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                   __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+}
+
+template <int L>
+__device__ __forceinline__ float leaf_sum_sqdev(const float (&v)[L], float mean) {  // same order, (v - mean)^2
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float d = __fsub_rn(v[j], mean);
+    r[j] = __fmul_rn(d, d);
+  }
+#pragma unroll
+  for (int i = 8; i < L; i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float d = __fsub_rn(v[i + j], mean);
+      r[j] = __fadd_rn(r[j], __fmul_rn(d, d));
+    }
+  return __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                   __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
+    zq_gemm2_ln_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const GemmParams p, const LnFuseParams f) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int COLS = BN / 2;  // one pairwise leaf
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sC = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + Cfg::EPI_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + STAGES;
+  uint64_t* tfull_bar = bars + 2 * STAGES;
+  uint64_t* tempty_bar = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  float* xch = reinterpret_cast<float*>(sC);  // [2][128] leaf partial exchange between the halves
+  unsigned int* sbase = reinterpret_cast<unsigned int*>(sC + 2048);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int tpr = f.tiles_per_round;
+  const int NT = p.num_n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full_bar[st], 2);
+      mbar_init(&empty_bar[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 2 * kNumEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = p.num_k_blocks;
+  pdl_trigger();
+
+  if (warp == 0) {
+    int stage = 0, phase = 0;
+    const int pre = (pair < tpr && pair < p.num_tiles) ? (nkb < STAGES ? nkb : STAGES) : 0;
+    if (lane == 0)
+      for (int kb = 0; kb < pre; ++kb) {
+        const uint32_t fb = leader_addr(&full_bar[kb]);
+        if (leader)
+          mbar_arrive_expect_tx(&full_bar[kb], 2 * Cfg::STAGE_BYTES);
+        else
+          mbar_arrive_cluster(fb);
+        tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, (pair % NT) * BN + rank * (BN / 2));
+      }
+    pdl_wait();
+    for (int tile = pair; pair < tpr && tile < p.num_tiles; tile += tpr) {
+      const int m0 = (tile / NT) * (2 * BLOCK_M) + rank * BLOCK_M;
+      const int n0 = (tile % NT) * BN + rank * (BN / 2);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (lane == 0) {
+          const uint32_t fb = leader_addr(&full_bar[stage]);
+          if (tile == pair && kb < pre) {
+            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+          } else {
+            if (leader)
+              mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+            else
+              mbar_arrive_cluster(fb);
+            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+            tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, n0);
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_i8(2 * BLOCK_M, BN);
+      int stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int tile = pair; pair < tpr && tile < p.num_tiles; tile += tpr) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BLOCK_K / 32; ++k)
+              mma_i8_cg2(d_tmem, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32), idesc,
+                         (kb | k) != 0);
+            mma_commit_mc2(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) mma_commit_mc2(&tfull_bar[acc], 0x3);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== fused epilogue =====================
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int rl = quarter * 32 + lane;  // row within the CTA's 128
+    int acc = 0, acc_phase = 0;
+    for (int tile = pair; pair < tpr && tile < p.num_tiles; tile += tpr) {
+      const int rb = tile / NT, nt = tile % NT;
+      const int row = rb * (2 * BLOCK_M) + rank * BLOCK_M + rl;
+      const bool live = row < p.M;
+      const int n0 = nt * BN + half * COLS;
+      const float s_tok = live ? __ldg(p.token_scales + row) : 0.0f;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
+      float v[COLS];
+      const float* xr = f.residual + (int64_t)(live ? row : 0) * p.N + n0;
+#pragma unroll
+      for (int c = 0; c < COLS; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 sw = __ldg(reinterpret_cast<const float4*>(p.row_scales + n0 + c + j));
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + c + j));
+          const float4 xx = live ? __ldg(reinterpret_cast<const float4*>(xr + c + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float swv[4] = {sw.x, sw.y, sw.z, sw.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+          const float xv[4] = {xx.x, xx.y, xx.z, xx.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float fo = __fadd_rn(__fmul_rn(__fmul_rn(__int2float_rn((int)r[j + u]), s_tok), swv[u]), bv[u]);
+            v[c + j + u] = __fadd_rn(xv[u], fo);  // x + f (transformer.py:477 / :486)
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty_bar[acc]));  // accumulator consumed
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+      unsigned int* cnt = f.counters + rb;
+      const unsigned int per_round = 2u * NT;
+      // exchange one value per (row, tile) through global memory, round `rd`
+      auto publish_and_wait = [&](int rd, float val) {
+        if (half == 0 && live) __stcg(f.partials + ((int64_t)rd * p.M + row) * NT + nt, val);
+        epi_bar();  // orders the CTA's partial stores before the releasing add below
+        if (warp == 2 && lane == 0) {
+          unsigned int old;
+          asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+          if (rd == 0) *sbase = old - old % (3u * per_round);
+          const unsigned int target = *sbase + (unsigned int)(rd + 1) * per_round;
+          while (!(p.debug & 4) && (int)(ld_acquire_u32(cnt) - target) < 0) __nanosleep(64);
+        }
+        epi_bar();
+      };
+      auto gather_tree = [&](int rd) -> float {  // balanced tree over the NT tile partials
+        const float* pr = f.partials + ((int64_t)rd * p.M + (live ? row : 0)) * NT;
+        if (NT == 4) {
+          const float4 t = __ldcg(reinterpret_cast<const float4*>(pr));
+          return __fadd_rn(__fadd_rn(t.x, t.y), __fadd_rn(t.z, t.w));
+        }
+        // larger NT: pairwise levels with a small stack of partial sums (binary counter)
+        float stk[7];
+        int cnt = 0;
+        for (int i = 0; i < NT; ++i) {
+          float val = __ldcg(pr + i);
+          int k = i;
+          // merge while the lowest bits of the index say a subtree completed
+          while (k & 1) {
+            val = __fadd_rn(stk[--cnt], val);
+            k >>= 1;
+          }
+          stk[cnt++] = val;
+        }
+        return stk[0];
+      };
+      // ---- round 0: mean ----
+      {
+        const float leaf = leaf_sum<COLS>(v);
+        xch[half * 128 + rl] = leaf;
+        epi_bar();
+        const float tsum = __fadd_rn(xch[rl], xch[128 + rl]);  // (left leaf + right leaf)
+        publish_and_wait(0, tsum);
+      }
+      const float fcols = (float)p.N;
+      const float mean = __fdiv_rn(gather_tree(0), fcols);
+      // ---- round 1: variance ----
+      {
+        const float leaf = leaf_sum_sqdev<COLS>(v, mean);
+        epi_bar();  // xch reuse
+        xch[half * 128 + rl] = leaf;
+        epi_bar();
+        publish_and_wait(1, __fadd_rn(xch[rl], xch[128 + rl]));
+      }
+      const float var = __fdiv_rn(gather_tree(1), fcols);
+      const float den = __fsqrt_rn(__fadd_rn(var, f.eps));
+      const float rden = __frcp_rn(den);
+      const bool den_ok = den > 1e-18f && den < 1e18f;
+      // ---- normalise, write y, row max ----
+      uint32_t ab = 0;
+      float* yr = f.ln_out + (int64_t)(live ? row : 0) * p.N + n0;
+#pragma unroll
+      for (int j = 0; j < COLS; j += 4) {
+        const float4 g = __ldg(reinterpret_cast<const float4*>(f.gamma + n0 + j));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(f.beta + n0 + j));
+        const float gv[4] = {g.x, g.y, g.z, g.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float a = __fsub_rn(v[j + u], mean);
+          float qd;
+          if (den_ok && (fabsf(a) >= 1e-30f || a == 0.0f)) {
+            const float q0 = __fmul_rn(a, rden);
+            const float q1 = __fmaf_rn(__fmaf_rn(-den, q0, a), rden, q0);
+            qd = __fmaf_rn(__fmaf_rn(-den, q1, a), rden, q1);
+          } else {
+            qd = __fdiv_rn(a, den);
+          }
+          v[j + u] = __fadd_rn(__fmul_rn(qd, gv[u]), bv[u]);
+          ab = max(ab, __float_as_uint(v[j + u]) & 0x7fffffffu);
+        }
+        if (live) *reinterpret_cast<float4*>(yr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      // ---- round 2: row max ----
+      epi_bar();
+      reinterpret_cast<uint32_t*>(xch)[half * 128 + rl] = ab;
+      epi_bar();
+      publish_and_wait(2, __uint_as_float(max(reinterpret_cast<uint32_t*>(xch)[rl],
+                                              reinterpret_cast<uint32_t*>(xch)[128 + rl])));
+      uint32_t amb_row = 0;
+      for (int i = 0; i < NT; ++i)
+        amb_row = max(amb_row, live ? __float_as_uint(__ldcg(f.partials + ((int64_t)2 * p.M + row) * NT + i)) : 0u);
+      if (!live) continue;
+      if (amb_row >= 0x7f800000u && nt == 0 && half == 0 && f.flag) atomicOr(f.flag, 1);
+      const float sc = scale_from_absmax(__uint_as_float(amb_row), f.qm);
+      const float inv = (__frcp_rn(sc) < 1e30f) ? __frcp_rn(sc) : 0.0f;
+      if (nt == 0 && half == 0) f.q_scales[row] = sc;
+      uint32_t* qrow = reinterpret_cast<uint32_t*>(f.q + (int64_t)row * f.ld_q + n0);
+#pragma unroll
+      for (int j = 0; j < COLS; j += 4) {
+        int o[4];
+        bool amb = inv == 0.0f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float m = __fmaf_rn(v[j + u], inv, 12582912.0f);
+          amb |= fabsf(__fmaf_rn(v[j + u], inv, -__fsub_rn(m, 12582912.0f))) > 0.5f - 6.103515625e-05f;
+          o[u] = __float_as_int(m) - 0x4B400000;
+        }
+        if (amb)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) o[u] = quantize_exact(v[j + u], sc, f.qm);
+        qrow[j / 4] = __byte_perm(__byte_perm((uint32_t)o[0], (uint32_t)o[1], 0x0040),
+                                  __byte_perm((uint32_t)o[2], (uint32_t)o[3], 0x0040), 0x5410);
+      }
+      if (nt == NT - 1 && half == 1)
+        for (int c = p.N; c < (int)f.ld_q; ++c) f.q[(int64_t)row * f.ld_q + c] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+}
+
+template <int BN>
+static int launch_gemm2_ln_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, const LnFuseParams& f,
+                             int grid, cudaStream_t st) {
+  using Cfg = Gemm2Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zq_gemm2_ln_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    attr = true;
+  }
+  const cudaError_t e = launch_kernel(zq_gemm2_ln_kernel<BN>, dim3(grid), dim3(Cfg::NUM_THREADS),
+                                      Cfg::SMEM_BYTES, st, 1, ta, tb, p, f);
+  if (e != cudaSuccess) {
+    set_error("fused linear + LN launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Standalone epilogue over an int32 accumulator (TP path) and the weight-only
 // FullAct GEMM (sequential f32 order, tensor.py:37-56).
@@ -1279,6 +1664,85 @@ int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float s
   const int kind = out_type == ZQ_OUT_F32 ? OUT_F32 : out_type == ZQ_OUT_F16 ? OUT_F16 : OUT_BF16;
   return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, kind, p,
                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zq_linear_ln_quantize(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq,
+                          int64_t ld_w, int w_bits, const float* w_row_scales, const float* bias, int64_t M,
+                          int64_t N, int64_t K, const float* residual, const float* gamma, const float* beta,
+                          float eps, int bits, float* ln_out, int8_t* q, int64_t ld_q, float* q_scales,
+                          void* workspace, int64_t workspace_bytes, int32_t* flag, void* stream) {
+  ZQ_CHECK_ARG(bits == 8 || bits == 4, ZQ_ERR_USAGE, "unsupported bit width %d", bits);
+  ZQ_CHECK_ARG(token_scales && w_row_scales && bias && residual && gamma && beta && ln_out && q && q_scales &&
+                   workspace,
+               ZQ_ERR_USAGE, "fused linear + LN needs every operand");
+  ZQ_CHECK_ARG(ld_q >= N && ld_q % 16 == 0, ZQ_ERR_USAGE, "bad quantized row stride");
+  // numpy's pairwise tree over N must be balanced with leaves of L <= 128 (L % 8 == 0):
+  // the pair tile is 2 leaves wide and NT = N / (2L) tiles (a power of two) span a row
+  int64_t L = N;
+  while (L > 128) {
+    if ((L / 2) % 8 != 0 || L % 2 != 0) return ZQ_ERR_UNSUPPORTED;
+    L /= 2;
+  }
+  if (w_bits != 8 || L % 8 != 0 || (L != 96 && L != 128) || N < 2 * L) return ZQ_ERR_UNSUPPORTED;
+  const int BN = (int)(2 * L);
+  const int NT = (int)(N / BN);
+  if ((NT & (NT - 1)) != 0 || NT > 64) return ZQ_ERR_UNSUPPORTED;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const int npairs = g_num_sms / 2;
+  if (NT > npairs) return ZQ_ERR_UNSUPPORTED;
+  const int64_t rblocks = (M + 255) / 256;
+  const int64_t need = (int64_t)sizeof(unsigned int) * rblocks + 16 + (int64_t)sizeof(float) * 3 * M * NT;
+  ZQ_CHECK_ARG(workspace_bytes >= need, ZQ_ERR_USAGE, "workspace too small (%lld < %lld bytes)",
+               (long long)workspace_bytes, (long long)need);
+  ZQ_CHECK_ARG(K * 127 * 127 < (1LL << 31), ZQ_ERR_USAGE, "igemm overflow guard");
+  ZQ_CHECK_ARG(ld_x >= K && ld_x % 16 == 0 && ld_w >= K && ld_w % 16 == 0, ZQ_ERR_USAGE, "bad operand strides");
+  if (!get_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ZQ_ERR_CUDA;
+  }
+  CUtensorMap ta, tb;
+  int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_tmap_u8(&tb, wq, N, K, ld_w, BLOCK_K, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.token_scales = token_scales;
+  p.row_scales = w_row_scales;
+  p.bias = bias;
+  p.num_n_tiles = NT;
+  p.num_tiles = (int)(rblocks * NT);
+  p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+  {
+    const char* e = getenv("ZQ_FUSE_DEBUG");  // diagnostics: 4 = skip the exchange waits (wrong results)
+    p.debug = e ? atoi(e) : 0;
+  }
+  LnFuseParams f;
+  f.residual = residual;
+  f.gamma = gamma;
+  f.beta = beta;
+  f.eps = eps;
+  f.ln_out = ln_out;
+  f.q = q;
+  f.ld_q = ld_q;
+  f.q_scales = q_scales;
+  f.qm = (1 << (bits - 1)) - 1;
+  f.counters = reinterpret_cast<unsigned int*>(workspace);
+  f.partials = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                        ((sizeof(unsigned int) * rblocks + 15) / 16) * 16);
+  f.flag = flag;
+  f.tiles_per_round = (npairs / NT) * NT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return BN == 192 ? launch_gemm2_ln_t<192>(ta, tb, p, f, 2 * npairs, st)
+                   : launch_gemm2_ln_t<256>(ta, tb, p, f, 2 * npairs, st);
 }
 
 int zq_dequant_epilogue(const int32_t* acc, int64_t ld_acc, const float* token_scales,

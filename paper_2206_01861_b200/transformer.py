@@ -22,6 +22,7 @@ outputs are compared with a tolerance (tests/test_transformer_gpu.py).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -466,7 +467,14 @@ class EncoderEngine:
             xq=quant.padded_int8(t, d), cq=quant.padded_int8(t, d), hq=quant.padded_int8(t, d),
             zq=quant.padded_int8(t, f), sx=e(t), sc=e(t), sh=e(t), sz=e(t),
             flag=torch.zeros(1, dtype=torch.int32, device=dev),
+            # fused linear + LN exchange workspaces (one per call site, zeroed once)
+            ws_o=torch.zeros(4 * ((t + 255) // 256) + 16 + 12 * t * 64, dtype=torch.uint8, device=dev),
+            ws_f=torch.zeros(4 * ((t + 255) // 256) + 16 + 12 * t * 64, dtype=torch.uint8, device=dev),
         )
+        # fused linear + LN measured slower than linear then LN at BERT shapes (the
+        # LN work runs on the GEMM's 8 epilogue warps per SM instead of a full-occupancy
+        # row kernel): opt-in with ZQ_FUSE_LN=1
+        self._fuse_ln = os.environ.get("ZQ_FUSE_LN", "0") == "1"
 
     @property
     def tokens(self) -> int:
@@ -479,6 +487,24 @@ class EncoderEngine:
         N.call("zq_linear", q.data_ptr(), q.stride(0), s.data_ptr(), 0.0, wp, ldw, wb,
                w.row_scales().data_ptr(), bias.data_ptr(), t, w.rows, k, out.data_ptr(), out.stride(0),
                N.OUT_F32, N.stream_ptr())
+
+    def _linear_ln(self, q, s, w: QuantizedMatrix, bias, res, g, b, ln_out, qo, so, ws) -> bool:
+        """linear + residual + LN + quantize in one kernel (zq_linear_ln_quantize);
+        False when the shape is not fusable (the caller runs the two kernels)."""
+        if not self._fuse_ln:
+            return False
+        t, k = q.shape
+        wp, ldw, wb = w.weight_operand()
+        rc = N.load().zq_linear_ln_quantize(
+            q.data_ptr(), q.stride(0), s.data_ptr(), wp, ldw, wb, w.row_scales().data_ptr(), bias.data_ptr(), t,
+            w.rows, k, res.data_ptr(), g.data_ptr(), b.data_ptr(), float(np.float32(LN_EPS)), 8, ln_out.data_ptr(),
+            qo.data_ptr(), qo.stride(0), so.data_ptr(), ws.data_ptr(), ws.numel(), self._bufs["flag"].data_ptr(),
+            N.stream_ptr())
+        if rc == N.ZQ_ERR_UNSUPPORTED:
+            self._fuse_ln = False
+            return False
+        N.check(rc)
+        return True
 
     def _ln_quant(self, x, res, g, b, ln_out, q, s):
         t, d = x.shape
@@ -517,13 +543,18 @@ class EncoderEngine:
             attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads, self.causal,
                       self.batch, out=B["ctx"])
             self._tok_quant(B["ctx"], B["cq"], B["sc"])
-            self._linear(B["cq"], B["sc"], blk.w_o, blk.b_o, B["attn"])
-            self._ln_quant(x, B["attn"], blk.ln1_gamma, blk.ln1_beta, B["h"], B["hq"], B["sh"])
+            # h = LN1(x + O-proj) and its quantization, fused into the O GEMM when possible
+            if not self._linear_ln(B["cq"], B["sc"], blk.w_o, blk.b_o, x, blk.ln1_gamma, blk.ln1_beta, B["h"],
+                                   B["hq"], B["sh"], B["ws_o"]):
+                self._linear(B["cq"], B["sc"], blk.w_o, blk.b_o, B["attn"])
+                self._ln_quant(x, B["attn"], blk.ln1_gamma, blk.ln1_beta, B["h"], B["hq"], B["sh"])
             self._linear(B["hq"], B["sh"], blk.w_h4h, blk.b_h4h, B["u"])
             self._gelu_quant(B["u"], B["zq"], B["sz"])
-            self._linear(B["zq"], B["sz"], blk.w_4hh, blk.b_4hh, B["f"])
             # y = LN2(h + f) is the next block's input; its quantization is fused
-            self._ln_quant(B["h"], B["f"], blk.ln2_gamma, blk.ln2_beta, x, xq, sx)
+            if not self._linear_ln(B["zq"], B["sz"], blk.w_4hh, blk.b_4hh, B["h"], blk.ln2_gamma, blk.ln2_beta, x,
+                                   xq, sx, B["ws_f"]):
+                self._linear(B["zq"], B["sz"], blk.w_4hh, blk.b_4hh, B["f"])
+                self._ln_quant(B["h"], B["f"], blk.ln2_gamma, blk.ln2_beta, x, xq, sx)
         self._ln_quant(x, None, self.final_gamma, self.final_beta, B["out"], B["cq"], B["sc"])
 
     def capture(self):

@@ -213,3 +213,44 @@ def test_skinny_decode_gemm_exact(zq, shape):
     out = igemm.fused_linear(xa, wm, bias)
     ref = O.dequant_epilogue(ref_acc, h(xa.token_scales), np.full(n, F32(0.003)), bias)
     assert bits_eq(h(out), ref), shape
+
+
+@pytest.mark.parametrize("shape", [(4096, 768, 768), (4096, 768, 3072), (300, 768, 768), (1000, 1024, 1024),
+                                   (600, 3072, 768)])
+def test_fused_linear_ln_quantize_matches_unfused(zq, shape):
+    """zq_linear_ln_quantize (GEMM + residual + LN + quantize in one kernel, row
+    statistics exchanged across CTAs) == zq_linear then zq_layer_norm_quantize,
+    bit for bit, over repeated launches sharing one workspace."""
+    from paper_2206_01861_b200 import _native as N
+
+    quant, igemm = zq
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k)
+    xa = make_qact(quant, rng.integers(-127, 128, (m, k)), scales=(rng.random(m) * 0.05 + 0.01).astype(F32))
+    w = quant.quantize_weight_groupwise((rng.standard_normal((n, k)) * 0.02).astype(F32), 16, 8)
+    bias = torch.from_numpy((rng.standard_normal(n) * 0.1).astype(F32)).cuda()
+    g = torch.from_numpy((1 + 0.1 * rng.standard_normal(n)).astype(F32)).cuda()
+    b = torch.from_numpy((0.1 * rng.standard_normal(n)).astype(F32)).cuda()
+    leaf = n
+    while leaf > 128:
+        leaf //= 2
+    nt = n // (2 * leaf)
+    ws = torch.zeros(4 * ((m + 255) // 256) + 16 + 12 * m * nt + 64, dtype=torch.uint8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    a = xa.gemm_operand()
+    wp, ldw, wb = w.weight_operand()
+    for it in range(3):
+        res = torch.from_numpy(rng.standard_normal((m, n)).astype(F32)).cuda()
+        y = torch.empty(m, n, device="cuda")
+        q = quant.padded_int8(m, n)
+        s = torch.empty(m, device="cuda")
+        N.call("zq_linear_ln_quantize", a.data_ptr(), a.stride(0), xa.token_scales.data_ptr(), wp, ldw, wb,
+               w.row_scales().data_ptr(), bias.data_ptr(), m, n, k, res.data_ptr(), g.data_ptr(), b.data_ptr(),
+               1e-5, 8, y.data_ptr(), q.data_ptr(), q.stride(0), s.data_ptr(), ws.data_ptr(), ws.numel(),
+               flag.data_ptr(), N.stream_ptr())
+        f = igemm.fused_linear(xa, w, bias)
+        y_ref = torch.empty(m, n, device="cuda")
+        qa = igemm.layer_norm_quantize(res, g, b, 8, residual=f, ln_out=y_ref)
+        assert bits_eq(h(y), h(y_ref)), (shape, it)
+        assert np.array_equal(h(q), h(qa.values)) and bits_eq(h(s), h(qa.token_scales)), (shape, it)
+    assert int(flag.item()) == 0
