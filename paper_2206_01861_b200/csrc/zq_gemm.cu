@@ -652,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
 // the rows across all S partials through distributed shared memory (exact: int32
 // addition is order-free) and applies the dequant epilogue for them.
 // ---------------------------------------------------------------------------
-constexpr int kSkStages = 4;
+constexpr int kSkStages = 4;  // 96 KB: two CTAs per SM (8 stages measured slower)
 
 template <int MP>
 struct SkinnyCfg {
@@ -1410,12 +1410,15 @@ static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmPar
   return ZQ_OK;
 }
 
+#ifndef ZQ_SKINNY_CTAS_PER_SM
+#define ZQ_SKINNY_CTAS_PER_SM 1  // grids of <= 1 CTA per SM leave room for the next launch (PDL); 2 measured slower
+#endif
 // Split-K degree: the largest S (<= 8) whose grid still fits one wave of two
 // CTAs per SM (a partial second wave costs more than the extra split saves) and
 // leaves every split >= 2 k-blocks.
 static int pick_split(int n_tiles, int nkb) {
   int S = 1;
-  while (S < 8 && n_tiles * S * 2 <= 2 * g_num_sms && nkb / (2 * S) >= 2) S *= 2;
+  while (S < 8 && n_tiles * S * 2 <= 2 * g_num_sms * ZQ_SKINNY_CTAS_PER_SM && nkb / (2 * S) >= 2) S *= 2;
   return S;
 }
 
