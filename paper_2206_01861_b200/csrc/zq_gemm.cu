@@ -654,13 +654,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
 // ---------------------------------------------------------------------------
 constexpr int kSkStages = 4;  // 96 KB: two CTAs per SM (8 stages measured slower)
 
-template <int MP>
+template <int MP, int W4 = 0>
 struct SkinnyCfg {
-  static constexpr int A_BYTES = 128 * BLOCK_K;   // weight tile
+  static constexpr int A_BYTES = 128 * BLOCK_K;   // weight tile (int8, SWIZZLE_128B)
   static constexpr int B_BYTES = MP * BLOCK_K;    // token tile
+  static constexpr int P_BYTES = W4 ? 128 * (BLOCK_K / 2) : 0;  // packed INT4 staging
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int PART_BYTES = MP * 128 * 4; // int32 partial [MP][128]
-  static constexpr int SMEM_BYTES = kSkStages * STAGE_BYTES + PART_BYTES + 256;
+  static constexpr int SMEM_BYTES = kSkStages * (STAGE_BYTES + P_BYTES) + PART_BYTES + 256;
 };
 
 __device__ __forceinline__ uint32_t dsmem_map(uint32_t addr, uint32_t rank) {
@@ -674,20 +675,25 @@ __device__ __forceinline__ int32_t dsmem_ld_s32(uint32_t addr) {
   return v;
 }
 
-template <int MP, int KIND>
+// W4: TMA brings the packed nibbles ([128 rows x 64 B], unswizzled) and warps 2-3
+// (idle during the main loop otherwise) unpack them into the int8 SWIZZLE_128B
+// tile the MMA reads, then add their arrivals on the stage's full barrier.
+template <int MP, int KIND, int W4>
 __global__ void __launch_bounds__(128, 1)
     zq_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                           const GemmParams p, int S) {
-  using Cfg = SkinnyCfg<MP>;
+  using Cfg = SkinnyCfg<MP, W4>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kSkStages * Cfg::A_BYTES;
-  int32_t* part = reinterpret_cast<int32_t*>(smem + kSkStages * Cfg::STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSkStages * Cfg::STAGE_BYTES + Cfg::PART_BYTES);
+  uint8_t* sP = smem + kSkStages * Cfg::STAGE_BYTES;  // W4 only
+  int32_t* part = reinterpret_cast<int32_t*>(smem + kSkStages * (Cfg::STAGE_BYTES + Cfg::P_BYTES));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSkStages * (Cfg::STAGE_BYTES + Cfg::P_BYTES) + Cfg::PART_BYTES);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + kSkStages;
   uint64_t* done_bar = bars + 2 * kSkStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kSkStages + 1);
+  uint64_t* praw_bar = bars + 2 * kSkStages + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kSkStages + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = (int)cluster_ctarank();
@@ -700,8 +706,9 @@ __global__ void __launch_bounds__(128, 1)
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     for (int st = 0; st < kSkStages; ++st) {
-      mbar_init(&full_bar[st], 1);
+      mbar_init(&full_bar[st], W4 ? 3 : 1);  // W4: + one arrival per unpack warp
       mbar_init(&empty_bar[st], 1);
+      if (W4) mbar_init(&praw_bar[st], 1);
     }
     mbar_init(done_bar, 1);
     fence_barrier_init();
@@ -717,19 +724,23 @@ __global__ void __launch_bounds__(128, 1)
     // the first kSkStages weight tiles stream in before the grid dependency resolves
     int stage = 0, phase = 0;
     const int pre = (kb1 - kb0) < kSkStages ? (kb1 - kb0) : kSkStages;
-    if (lane == 0)
-      for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
-        tma_load_2d(sA + i * Cfg::A_BYTES, &tmW, &full_bar[i], (kb0 + i) * BLOCK_K, n0);
+    auto load_w = [&](int st, int kb) {
+      if (W4) {
+        mbar_arrive_expect_tx(&praw_bar[st], Cfg::P_BYTES);
+        tma_load_2d(sP + st * Cfg::P_BYTES, &tmW, &praw_bar[st], kb * (BLOCK_K / 2), n0);
+        mbar_arrive_expect_tx(&full_bar[st], Cfg::B_BYTES);
+      } else {
+        mbar_arrive_expect_tx(&full_bar[st], Cfg::STAGE_BYTES);
+        tma_load_2d(sA + st * Cfg::A_BYTES, &tmW, &full_bar[st], kb * BLOCK_K, n0);
       }
+    };
+    if (lane == 0)
+      for (int i = 0; i < pre; ++i) load_w(i, kb0 + i);
     pdl_wait();
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&empty_bar[stage], phase ^ 1);
       if (lane == 0) {
-        if (kb - kb0 >= pre) {
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmW, &full_bar[stage], kb * BLOCK_K, n0);
-        }
+        if (kb - kb0 >= pre) load_w(stage, kb);
         tma_load_2d(sB + stage * Cfg::B_BYTES, &tmX, &full_bar[stage], kb * BLOCK_K, 0);
       }
       __syncwarp();
@@ -764,6 +775,40 @@ __global__ void __launch_bounds__(128, 1)
       else mbar_arrive(done_bar);  // empty split: contributes zeros
     }
     __syncwarp();
+  } else if (W4) {
+    // warps 2-3: INT4 -> INT8 into the SWIZZLE_128B tile (row r, 16-byte chunk c at
+    // r*128 + ((c ^ (r & 7)) * 16)); nibble j of a packed word is element j
+    const int ut = threadIdx.x - 64;
+    int stage = 0, phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&empty_bar[stage], phase ^ 1);
+      mbar_wait(&praw_bar[stage], phase);
+      const uint8_t* src = sP + stage * Cfg::P_BYTES;
+      uint8_t* dst = sA + stage * Cfg::A_BYTES;
+#pragma unroll 4
+      for (int idx = ut; idx < 128 * 8; idx += 64) {
+        const int rr = idx >> 3, c = idx & 7;
+        const uint2 pk = *reinterpret_cast<const uint2*>(src + rr * 64 + c * 8);
+        uint32_t w[4];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t x = hh ? pk.y : pk.x;
+          uint32_t ev = x & 0x0F0F0F0Fu, od = (x >> 4) & 0x0F0F0F0Fu;
+          ev |= (ev & 0x08080808u) * 0x1Eu;
+          od |= (od & 0x08080808u) * 0x1Eu;
+          w[2 * hh] = __byte_perm(ev, od, 0x5140);
+          w[2 * hh + 1] = __byte_perm(ev, od, 0x7362);
+        }
+        *reinterpret_cast<uint4*>(dst + rr * 128 + ((c ^ (rr & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[stage]);
+      if (++stage == kSkStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
   }
   // ---- partial: TMEM (lane = weight row) -> smem [MP][128] ----
   mbar_wait(done_bar, 0);
@@ -1391,17 +1436,17 @@ static int pick_bn(int64_t M, int64_t N) {
   return 64;
 }
 
-template <int MP, int KIND>
+template <int MP, int KIND, int W4>
 static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmParams p, int S,
                            cudaStream_t st) {
-  using Cfg = SkinnyCfg<MP>;
+  using Cfg = SkinnyCfg<MP, W4>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(zq_gemm_skinny_kernel<MP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zq_gemm_skinny_kernel<MP, KIND, W4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
     attr = true;
   }
-  cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND>, dim3(p.num_n_tiles * S), dim3(128),
+  cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND, W4>, dim3(p.num_n_tiles * S), dim3(128),
                                 Cfg::SMEM_BYTES, st, S, tw, tx, p, S);
   if (e != cudaSuccess) {
     set_error("skinny gemm launch: %s", cudaGetErrorString(e));
@@ -1422,11 +1467,12 @@ static int pick_split(int n_tiles, int nkb) {
   return S;
 }
 
-static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int64_t M,
+static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits, int64_t M,
                        int64_t N, int64_t K, int kind, GemmParams p, cudaStream_t st) {
   const int MP = M <= 32 ? 32 : 64;
   CUtensorMap tw, tx;
-  int rc = make_tmap_u8(&tw, wq, N, K, ld_w, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  int rc = w_bits == 8 ? make_tmap_u8(&tw, wq, N, K, ld_w, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B)
+                       : make_tmap_u8(&tw, wq, N, ld_w / 2, ld_w / 2, BLOCK_K / 2, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (rc) return rc;
   rc = make_tmap_u8(&tx, xq, M, K, ld_x, BLOCK_K, MP, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
@@ -1437,7 +1483,9 @@ static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
   p.num_tiles = p.num_n_tiles;
   const int S = pick_split(p.num_n_tiles, p.num_k_blocks);
-#define ZQ_SK(KK) (MP == 32 ? launch_skinny_t<32, KK>(tw, tx, p, S, st) : launch_skinny_t<64, KK>(tw, tx, p, S, st))
+#define ZQ_SK(KK)                                                                               \
+  (w_bits == 4 ? (MP == 32 ? launch_skinny_t<32, KK, 1>(tw, tx, p, S, st) : launch_skinny_t<64, KK, 1>(tw, tx, p, S, st)) \
+               : (MP == 32 ? launch_skinny_t<32, KK, 0>(tw, tx, p, S, st) : launch_skinny_t<64, KK, 0>(tw, tx, p, S, st)))
   switch (kind) {
     case OUT_S32: return ZQ_SK(OUT_S32);
     case OUT_F32: return ZQ_SK(OUT_F32);
@@ -1483,8 +1531,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
     const char* e = getenv("ZQ_GEMM_SKINNY");
     skinny_mode = e ? atoi(e) : 1;
   }
-  if (w_bits == 8 && M <= 64 && skinny_mode != 0)
-    return gemm_skinny(xq, ld_x, wq, ld_w, M, N, K, kind, p, st);
+  if (M <= 64 && skinny_mode != 0) return gemm_skinny(xq, ld_x, wq, ld_w, w_bits, M, N, K, kind, p, st);
   // CTA-pair path for int8 weights when there are enough 256-row tiles to fill
   // the machine (ZQ_GEMM_PAIR=0 disables, =1 forces where legal)
   static int pair_mode = -1;

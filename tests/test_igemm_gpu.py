@@ -254,3 +254,20 @@ def test_fused_linear_ln_quantize_matches_unfused(zq, shape):
         assert bits_eq(h(y), h(y_ref)), (shape, it)
         assert np.array_equal(h(q), h(qa.values)) and bits_eq(h(s), h(qa.token_scales)), (shape, it)
     assert int(flag.item()) == 0
+
+
+@pytest.mark.parametrize("shape", [(1, 1024, 4096), (8, 4096, 1024), (16, 4096, 16384), (64, 768, 3072), (5, 160, 200)])
+def test_skinny_decode_gemm_w4_exact(zq, shape):
+    """W4A8 at decode sizes: packed INT4 tiles unpacked in smem by the skinny kernel."""
+    quant, igemm = zq
+    t, d, n = shape
+    rng = np.random.default_rng(7 * sum(shape))
+    xv = rng.integers(-127, 128, (t, d)).astype(np.int8)
+    wv = rng.integers(-7, 8, (n, d)).astype(np.int8)
+    xa = make_qact(quant, xv, scales=rng.random(t).astype(F32) + 0.01)
+    wm = make_qmat(quant, wv, scales=(0.01,), bits=4)
+    acc = igemm.igemm(xa, wm)
+    ref_acc = O.igemm(xv, wv)
+    assert np.array_equal(h(acc.acc), ref_acc), shape
+    out = igemm.fused_linear(xa, wm, None)
+    assert bits_eq(h(out), O.dequant_epilogue(ref_acc, h(xa.token_scales), np.full(n, F32(0.01)), None)), shape
