@@ -191,6 +191,11 @@ int zq_gemm_set_trace(unsigned long long* buf);
  * CTA (phase boundaries) into ctx instead of its output; 0 = normal. */
 int zq_attention_debug(int mode);
 
+/* Diagnostics: when buf != NULL, the short-sequence attention kernel records
+ * %globaltimer stamps buf[cta*64 + head_iter*8 + phase] (phase 0 loop start,
+ * 1 operands landed, 2 split done, 3 S done, 4 P in TMEM, 5 O done, 6 stored). */
+int zq_attention_set_trace(unsigned long long* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ _SIGS = {
     "zq_quantize_with_absmax": [_p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p],
     "zq_gemm_set_trace": [_p],
     "zq_attention_debug": [_i32],
+    "zq_attention_set_trace": [_p],
     "zq_gelu_estimate": [_p, _i64, _p, _p, _p],
     "zq_attention_f32": [_p, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _p, _i64, _p],
     "zq_kv_append": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _p],

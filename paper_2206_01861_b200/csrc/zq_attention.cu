@@ -29,6 +29,7 @@
 //      (M=128, N=64, K=128) -> TMEM cols [256,320);
 //   6. 8 warps read O and store ctx rows (f32).
 #include <cuda.h>
+#include <string.h>
 
 #include "zq_common.cuh"
 
@@ -156,7 +157,9 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // V load goes out as soon as V has been transposed.
 __global__ void __launch_bounds__(256, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tm, int seq, int heads, int dmodel,
-                     int causal, float scale, float* __restrict__ ctx, int64_t ld_ctx, int nheads_total) {
+                     int causal, float scale, float* __restrict__ ctx, int64_t ld_ctx, int nheads_total,
+                     unsigned long long* __restrict__ trace, const __grid_constant__ CUtensorMap tmc,
+                     int tma_store) {
   // no static smem in this kernel: the dynamic window starts 1024-aligned, and
   // addressing it directly (no integer round trip) keeps every access LDS/STS
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -211,12 +214,19 @@ __global__ void __launch_bounds__(256, 1)
     issue_v(blockIdx.x);
   }
   int it = 0;
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
   for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
     const uint32_t ph = it & 1;
+    if (tr && it < 8) tr[it * 8 + 0] = gtime();
     const int nxt = hd + gridDim.x;
     const int b = hd / heads, h = hd % heads;
     mbar_wait(&bar[1], ph);
     mbar_wait(&bar[0], ph);
+    if (tma_store && it > 0) {  // the previous head's O staging (in lo(K)) must be read out
+      if (tid == 0) bulk_wait_read0();
+      __syncthreads();
+    }
+    if (tr && it < 8) tr[it * 8 + 1] = gtime();
     // ---- lo(Q), lo(K) in place; V -> K-major V^T hi / lo ----
     for (int i = tid; i < 2 * (kRegion / 16); i += 256) {
       const int part = i / (kRegion / 16), off = (i % (kRegion / 16)) * 16;
@@ -255,6 +265,7 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 2] = gtime();
     if (tid == 0 && nxt < nheads_total) issue_v(nxt);  // V raw is free again
 
     // ---- S = Q K^T (3-term split) -> TMEM [0,128) ----
@@ -275,6 +286,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(&bar[2], ph);
     tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 3] = gtime();
     if (tid == 0 && nxt < nheads_total) issue_qk(nxt);  // Q / K are consumed
 
     // ---- softmax rows: S from TMEM, P hi / lo back into TMEM ----
@@ -329,6 +341,7 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 4] = gtime();
 
     // ---- O = P V (3-term split), A = P from TMEM, N = 64 -> TMEM [256,320) ----
     if (warp == 0) {
@@ -347,11 +360,20 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(&bar[3], ph);
     tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 5] = gtime();
     {
       uint32_t r0[32];
       tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16) + 256 + half * 32, r0);
       tmem_ld_wait();
-      if (row < seq) {
+      if (tma_store) {
+        // stage O in lo(K) (dead after S) as two [128 rows x 32 cols] SWIZZLE_128B
+        // boxes; one bulk tensor store per box drains while the next head runs
+        uint8_t* st = sKl + half * (kRegion / 2) + row * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(st + ((c ^ (row & 7)) << 4)) =
+              make_uint4(r0[4 * c], r0[4 * c + 1], r0[4 * c + 2], r0[4 * c + 3]);
+      } else if (row < seq) {
         float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
 #pragma unroll
         for (int j = 0; j < 32; j += 4)
@@ -360,10 +382,18 @@ __global__ void __launch_bounds__(256, 1)
                           __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
       }
     }
+    if (tma_store) fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();  // TMEM / smem of this head are free for the next one
     tc_fence_after();
+    if (tma_store && tid == 0) {
+      tma_store_2d(&tmc, sKl, h * kAttD, b * seq);
+      tma_store_2d(&tmc, sKl + kRegion / 2, h * kAttD + 32, b * seq);
+      bulk_commit();
+    }
+    if (tr && it < 8) tr[it * 8 + 6] = gtime();
   }
+  if (tma_store && tid == 0) bulk_wait0();  // ctx stores complete before exit
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
@@ -660,8 +690,13 @@ int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols,
 
 using namespace zq;
 
-extern "C" int zq_attention_debug(int mode) {  // phase stamps were removed with the persistent kernel
+static unsigned long long* g_att_trace = nullptr;
+extern "C" int zq_attention_debug(int mode) {  // kept for ABI stability; see zq_attention_set_trace
   return mode == 0 ? ZQ_OK : ZQ_ERR_UNSUPPORTED;
+}
+extern "C" int zq_attention_set_trace(unsigned long long* buf) {
+  g_att_trace = buf;
+  return ZQ_OK;
 }
 
 extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads,
@@ -692,8 +727,17 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   cudaError_t e;
   if (seq <= kAttT) {
     const int grid = total < nsm ? total : nsm;
+    // seq == 128: whole 128-row boxes belong to one sequence, so O leaves by bulk TMA stores
+    CUtensorMap tmc;
+    int tma_store = 0;
+    if (seq == kAttT && (ld_ctx * 4) % 16 == 0) {
+      tma_store = make_tmap_f32(&tmc, ctx, (int64_t)batch * seq, (int64_t)heads * head_dim, ld_ctx * 4, 32, kAttT,
+                                CU_TENSOR_MAP_SWIZZLE_128B) == ZQ_OK;
+    }
+    if (!tma_store) memset(&tmc, 0, sizeof(tmc));
     e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem, reinterpret_cast<cudaStream_t>(stream),
-                      1, tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, total);
+                      1, tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
+                      tma_store);
   } else {
     const int nq = (seq + kAttT - 1) / kAttT;
     const int items = total * nq;
