@@ -81,26 +81,32 @@ inline bool bits_ok(int bits) { return bits == 4 || bits == 8; }
 // ---------------------------------------------------------------------------
 
 // Scale from a row max (quant.py:222-226): f32(f64(maxabs) / qmax), 0 -> 1.0.
-// f64 division and the single cvt.rn.f32.f64 are exactly numpy's arithmetic.
+// That double rounding equals one correctly rounded f32 division: for f32 a and
+// odd qm (127, 7) the exact quotient a/qm is never an f32 rounding midpoint and
+// stays >= 2^-32 (relative) away from every midpoint (the numerator
+// a*2^k - qm*(2j+1) is a nonzero integer multiple of the midpoint grid), far
+// beyond the f64 quotient's 2^-53 error, so RN_f32(RN_f64(a/qm)) = RN_f32(a/qm)
+// (also for subnormal a).  The f32 IEEE division keeps the FP64 pipe (slow on
+// this part) off every row's critical path.
 __device__ __forceinline__ float scale_from_absmax(float amax, int qm) {
   if (amax == 0.0f) return 1.0f;
-  return __double2float_rn(__ddiv_rn((double)amax, (double)qm));
+  return __fdiv_rn(amax, (float)qm);
 }
 
 // q = clamp(sign(x) * floor(|x|/s + 1/2), +-qm) for f32 x and f32 s > 0.
 // The reference divides in f64; for f32 operands its result equals exact
 // round-half-away of the rational |x|/s (the f64 quotient cannot cross a
 // half-integer it is not exactly on).  We estimate k from an f32 quotient and
-// fix it with an exact f64 boundary test: (k -+ 1/2) * s is exact in f64
-// (24-bit s times a <=10-bit half-integer).
+// fix it with an exact boundary test on (k -+ 1/2) * s.
 __device__ __forceinline__ int quantize_exact(float x, float s, int qm) {
   float ax = fabsf(x);
   float r = fminf(__fdiv_rn(ax, s), 512.0f);
   int k = __float2int_rd(__fadd_rn(r, 0.5f));
-  double axd = (double)ax, sd = (double)s;
-  if (__dmul_rn((double)k - 0.5, sd) > axd) {
+  // (k -+ 1/2) * s - |x| with a single rounding (FMA): its sign is the sign of the
+  // exact value (zero stays zero), so the boundary tests are exact in f32
+  if (__fmaf_rn((float)k - 0.5f, s, -ax) > 0.0f) {
     k -= 1;
-  } else if (__dmul_rn((double)k + 0.5, sd) <= axd) {
+  } else if (__fmaf_rn((float)k + 0.5f, s, -ax) <= 0.0f) {
     k += 1;
   }
   k = min(k, qm);
