@@ -331,19 +331,35 @@ def run_ours(args, rank: int, world: int, dist):
     eng.check_finite()
 
     # ---- end to end through the public API with host buffers ----
-    out_host = torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32).pin_memory()
-    e2e_times = []
+    # Every step: pinned-host ids H2D (inside forward()), the forward, and a D2H of
+    # the step's hidden states.  The D2H of step i runs on a copy stream from a
+    # device snapshot while step i+1 computes (the serving pipeline); the timed
+    # region spans all steps, L2 flushes included.
+    out_host = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32).pin_memory() for _ in range(2)]
+    snap = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32, device="cuda") for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    copied = [None, None]
     barrier()
-    for _ in range(args.steps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(args.steps):
         flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
         out = eng.forward(ids_host)          # H2D of ids inside
-        out_host.copy_(out, non_blocking=True)  # D2H of the result
-        b.record(stream)
-        e2e_times.append((a, b))
+        j = i % 2
+        if copied[j] is not None:
+            stream.wait_event(copied[j])     # the D2H that read snap[j] is done
+        snap[j].copy_(out)
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        copy_stream.wait_event(ready)
+        with torch.cuda.stream(copy_stream):
+            out_host[j].copy_(snap[j], non_blocking=True)  # D2H of the result
+        copied[j] = torch.cuda.Event()
+        copied[j].record(copy_stream)
+    stream.wait_stream(copy_stream)
+    b.record(stream)
     barrier()
-    e2e_total = sum(a.elapsed_time(b) * 1e-3 for a, b in e2e_times)
+    e2e_total = a.elapsed_time(b) * 1e-3
 
     if dist is not None:
         t = torch.tensor([total, e2e_total], device="cuda", dtype=torch.float64)
@@ -367,7 +383,8 @@ def run_ours(args, rank: int, world: int, dist):
         "vs_baseline": None, "dtype": "int8", "data": "synthetic (random-init weights, random token ids)",
         "config": workload_config(),
         "e2e": {"value": e2e_value, "unit": "seq/s", "h2d_bytes_per_step": int(ids_host.numel() * 8),
-                "d2h_bytes_per_step": int(out_host.numel() * 4)},
+                "d2h_bytes_per_step": int(out_host[0].numel() * 4),
+                "pipeline": "D2H of step i overlaps step i+1 on a copy stream; L2 flushes inside the timed region"},
         "roofline": roof,
         "cpu_baseline": {"value": cpu_val, "unit": "seq/s", "cores": cores, "kind": "port", "sample": cpu_sample},
         "gpu_launches": launches_per_step * args.steps,
