@@ -48,10 +48,34 @@ struct GemmParams {
   int tma_out;                // output tensor map valid -> staged TMA stores
   unsigned long long* trace;  // diagnostics: per-CTA %globaltimer stamps (nullable)
   int debug;                  // diagnostics: 1 = skip global stores, 2 = skip dequant math
+  int group_m;                // tile rasterisation group (1 = row-major)
 };
 
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
+// Grouped tile rasterisation: consecutive tile ids walk kGroupM m-blocks before
+// moving to the next n-block, so the ~1 wave of concurrently active tiles covers
+// kGroupM x (CTAs / kGroupM) tiles and the A / B panels they share stay in L2
+// (row-major order re-read all of B from DRAM once per 2-3 m-blocks: 711 MB of
+// DRAM reads for the 128 MB of operands of an 8192^3 GEMM).
+// Output-bound GEMMs (small K, e.g. BERT's K = 768) keep plain row-major order
+// (group 1: concurrent tiles share output rows, which the f32 stores favour).
+__device__ __forceinline__ void tile_coords(int tile, int num_m_tiles, int num_n_tiles, int group_m, int& mt,
+                                            int& nt) {
+  const int per_group = group_m * num_n_tiles;
+  const int g = tile / per_group, r = tile % per_group;
+  const int gm = min(group_m, num_m_tiles - g * group_m);
+  mt = g * group_m + r % gm;
+  nt = r / gm;
+}
+
+template <int BN, typename P>
+__device__ __forceinline__ int tile_n0(int tile, const P& p) {
+  int mt, nt;
+  tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+  return nt * BN;
 }
 
 template <int BN, int W4>
@@ -233,12 +257,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
       for (int kb = 0; kb < pre; ++kb) {
         mbar_arrive_expect_tx(&full_bar[kb], Cfg::STAGE_BYTES);
         tma_load_2d(sB + kb * Cfg::B_BYTES, &tmB, &full_bar[kb], kb * BLOCK_K,
-                    ((int)blockIdx.x % p.num_n_tiles) * BN);
+                    tile_n0<BN>(blockIdx.x, p));
       }
     pdl_wait();
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
-      const int n0 = (tile % p.num_n_tiles) * BN;
+      int mt, nt;
+      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      const int m0 = mt * BLOCK_M;
+      const int n0 = nt * BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
@@ -315,8 +341,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
-      const int m0 = (tile / p.num_n_tiles) * BLOCK_M;
-      const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
+      int mt, nt;
+      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      const int m0 = mt * BLOCK_M;
+      const int n0 = nt * BN + half * COLS;
       const int row0 = m0 + quarter * 32;
       const int row = row0 + lane;
       float s_tok = p.static_scale;
@@ -508,12 +536,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
         else
           mbar_arrive_cluster(fb);
         tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K,
-                        (pair % p.num_n_tiles) * BN + rank * (BN / 2));
+                        tile_n0<BN>(pair, p) + rank * (BN / 2));
       }
     pdl_wait();
     for (int tile = pair; tile < p.num_tiles; tile += npairs) {
-      const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
-      const int n0 = (tile % p.num_n_tiles) * BN + rank * (BN / 2);
+      int mt, nt;
+      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      const int m0 = mt * (2 * BLOCK_M) + rank * BLOCK_M;
+      const int n0 = nt * BN + rank * (BN / 2);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
@@ -585,8 +615,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
-      const int m0 = (tile / p.num_n_tiles) * (2 * BLOCK_M) + rank * BLOCK_M;
-      const int n0 = (tile % p.num_n_tiles) * BN + half * COLS;
+      int mt, nt;
+      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      const int m0 = mt * (2 * BLOCK_M) + rank * BLOCK_M;
+      const int n0 = nt * BN + half * COLS;
       const int row0 = m0 + quarter * 32;
       const int row = row0 + lane;
       float s_tok = p.static_scale;
@@ -1602,6 +1634,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.num_n_tiles = (int)((N + bn2 - 1) / bn2);
       p.num_tiles = (int)mp * p.num_n_tiles;
       p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+      p.group_m = K >= 2048 ? 8 : 1;  // operand-bound: keep A / B panels in L2
 #define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, tc, p, st) \
                    : bn2 == 192 ? launch_gemm2_t<192, KK>(ta, tb, tc, p, st)  \
                                 : launch_gemm2_t<128, KK>(ta, tb, tc, p, st))
@@ -1661,6 +1694,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   p.num_n_tiles = (int)((N + bn - 1) / bn);
   p.num_tiles = (int)((M + BLOCK_M - 1) / BLOCK_M) * p.num_n_tiles;
   p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
+  p.group_m = K >= 2048 ? 8 : 1;
   const bool w4 = w_bits == 4;
   switch (kind) {
     case OUT_S32: return w4 ? launch_gemm_bn<OUT_S32, 1>(bn, ta, tb, tc, p, st) : launch_gemm_bn<OUT_S32, 0>(bn, ta, tb, tc, p, st);
