@@ -187,19 +187,16 @@ __device__ __forceinline__ T warp_max(T v) {
 // non-negative floats, NaN never reaches here because the finite flag is raised
 // separately).  `red` must hold >= 32 words.
 __device__ __forceinline__ float block_max_nonneg(float v, uint32_t* red) {
-  uint32_t b = warp_max(__float_as_uint(v));
-  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // redux.sync per warp, one slot per warp, then every warp reduces the slots
+  // itself (two barriers; the leading one protects the slots of the last call)
+  uint32_t b = __reduce_max_sync(0xffffffffu, __float_as_uint(v));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
   if (l == 0) red[w] = b;
   __syncthreads();
-  int nw = (blockDim.x + 31) >> 5;
-  b = (threadIdx.x < nw) ? red[threadIdx.x] : 0u;
-  if (w == 0) {
-    b = warp_max(b);
-    if (l == 0) red[0] = b;
-  }
-  __syncthreads();
-  return __uint_as_float(red[0]);
+  const int nw = (blockDim.x + 31) >> 5;
+  b = l < nw ? red[l] : 0u;
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, b));
 }
 
 // ---------------------------------------------------------------------------
