@@ -14,7 +14,7 @@ import threading
 from .errors import ShapeError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzq_b200.so")
+LIB_PATH = os.environ.get("ZQ_LIB") or os.path.join(_HERE, "libzq_b200.so")  # ZQ_LIB: experiment builds
 
 ZQ_OK, ZQ_ERR_USAGE, ZQ_ERR_SHAPE, ZQ_ERR_CUDA, ZQ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 OUT_F32, OUT_F16, OUT_BF16 = 0, 1, 2

@@ -363,6 +363,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1)
       : "memory");
 }
+// The same, multicast: the tile lands at the same offset in every CTA of
+// `mask`, and each destination's pair leader barrier receives its bytes.
+__device__ __forceinline__ void tma_load_2d_cg2_mc(void* smem_dst, const void* tmap, uint32_t bar_leader,
+                                                   int32_t c0, int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(dst_smem)),

@@ -456,6 +456,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, W4>::NUM_THREADS, 1)
 //   empty_bar  (each)  : multicast tcgen05.commit from the leader
 //   tfull_bar  (each)  : multicast commit after a tile's last MMA
 //   tempty_bar (leader): 2 x kNumEpiWarps arrivals (both CTAs' epilogue warps)
+// CL = 4: a cluster of two pairs computes a 256 x 2BN unit (pair s = rank >> 1
+// takes n-tile 2u + s); the pairs share A, so each A k-block is loaded once and
+// multicast to the two CTAs holding those rows (the pairs alternate k-blocks as
+// issuer), halving A's L2->SM traffic, which bounds the operand-fed phase.
+// Both pairs' MMA commits release every CTA's stage (empty_bar counts 2), so a
+// multicast never overwrites a slot the other pair still reads.
 // ---------------------------------------------------------------------------
 template <int BN>
 struct Gemm2Cfg {
@@ -473,8 +479,8 @@ struct Gemm2Cfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
-template <int BN, int KIND>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
+template <int BN, int KIND, int CL>
+__global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
     zq_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
@@ -494,9 +500,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;  // rank within the pair
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int sub = CL == 4 ? (int)(crank >> 1) : 0;  // pair within the cluster
+  const int unit0 = blockIdx.x / CL, nunits_grid = gridDim.x / CL;
+  constexpr int NSUB = CL / 2;
+  const int num_m_tiles = p.num_tiles / p.num_n_tiles;
+  const int num_nu = (p.num_n_tiles + NSUB - 1) / NSUB;  // n-units
+  const int num_units = num_m_tiles * num_nu;
+  auto unit_coords = [&](int u, int& mt, int& nt) {
+    int ntu;
+    tile_coords(u, num_m_tiles, num_nu, p.group_m, mt, ntu);
+    nt = ntu * NSUB + sub;
+  };
   unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtime();
 
@@ -506,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 2);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], NSUB);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -527,35 +544,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     // ===================== TMA producer (both CTAs) =====================
     // weight halves of the first tile's stages go out before the grid dependency
     int stage = 0, phase = 0;
-    const int pre = pair < p.num_tiles ? (nkb < STAGES ? nkb : STAGES) : 0;
-    if (lane == 0)
+    const int pre = unit0 < num_units ? (nkb < STAGES ? nkb : STAGES) : 0;
+    // CL = 4: this CTA loads (and multicasts) A for k-blocks kb with kb % 2 == sub
+    const uint16_t amask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+    auto load_a = [&](int st_, int kb, int m0, uint32_t fb) {
+      if (CL == 2)
+        tma_load_2d_cg2(sA + st_ * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+      else if ((kb & 1) == sub)
+        tma_load_2d_cg2_mc(sA + st_ * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0, amask);
+    };
+    if (lane == 0 && pre) {
+      int mt, nt;
+      unit_coords(unit0, mt, nt);
       for (int kb = 0; kb < pre; ++kb) {
         const uint32_t fb = leader_addr(&full_bar[kb]);
         if (leader)
           mbar_arrive_expect_tx(&full_bar[kb], 2 * Cfg::STAGE_BYTES);
         else
           mbar_arrive_cluster(fb);
-        tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K,
-                        tile_n0<BN>(pair, p) + rank * (BN / 2));
+        tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, nt * BN + rank * (BN / 2));
       }
+    }
     pdl_wait();
-    for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+    for (int u = unit0; u < num_units; u += nunits_grid) {
       int mt, nt;
-      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      unit_coords(u, mt, nt);
       const int m0 = mt * (2 * BLOCK_M) + rank * BLOCK_M;
       const int n0 = nt * BN + rank * (BN / 2);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = leader_addr(&full_bar[stage]);
-          if (tile == pair && kb < pre) {
-            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+          if (u == unit0 && kb < pre) {
+            load_a(stage, kb, m0, fb);
           } else {
             if (leader)
               mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
             else
               mbar_arrive_cluster(fb);
-            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * BLOCK_K, m0);
+            load_a(stage, kb, m0, fb);
             tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * BLOCK_K, n0);
           }
         }
@@ -571,7 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     if (leader) {
       constexpr uint32_t idesc = make_idesc_i8(2 * BLOCK_M, BN);
       int stage = 0, phase = 0, acc = 0, acc_phase = 0, lt = 0;
-      for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
+      for (int u = unit0; u < num_units; u += nunits_grid, ++lt) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         if (tr && lane == 0 && lt < 15) tr[2 + 4 * lt] = gtime();
@@ -587,7 +614,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
             for (int k = 0; k < BLOCK_K / 32; ++k)
               mma_i8_cg2(d_tmem, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32),
                          idesc, (kb | k) != 0);
-            mma_commit_mc2(&empty_bar[stage], 0x3);
+            mma_commit_mc2(&empty_bar[stage], CL == 4 ? 0xF : 0x3);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -595,7 +622,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
             phase ^= 1;
           }
         }
-        if (lane == 0) mma_commit_mc2(&tfull_bar[acc], 0x3);
+        if (lane == 0) mma_commit_mc2(&tfull_bar[acc], (uint16_t)(0x3u << (crank & 2)));
         __syncwarp();
         if (++acc == 2) {
           acc = 0;
@@ -614,9 +641,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::NUM_TH
     if (p.tma_out && lane == 0) prefetch_tmap(&tmC);
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
-    for (int tile = pair; tile < p.num_tiles; tile += npairs, ++lt) {
+    for (int u = unit0; u < num_units; u += nunits_grid, ++lt) {
       int mt, nt;
-      tile_coords(tile, p.num_tiles / p.num_n_tiles, p.num_n_tiles, p.group_m, mt, nt);
+      unit_coords(u, mt, nt);
       const int m0 = mt * (2 * BLOCK_M) + rank * BLOCK_M;
       const int n0 = nt * BN + half * COLS;
       const int row0 = m0 + quarter * 32;
@@ -1422,19 +1449,42 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   return ZQ_OK;
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int CL>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, GemmParams p,
                           cudaStream_t st) {
   using Cfg = Gemm2Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(zq_gemm2_kernel<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zq_gemm2_kernel<BN, KIND, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
     attr = true;
   }
-  const int pairs = p.num_tiles < g_num_sms / 2 ? p.num_tiles : g_num_sms / 2;
-  const cudaError_t e = launch_kernel(zq_gemm2_kernel<BN, KIND>, dim3(2 * pairs), dim3(Cfg::NUM_THREADS),
-                                      Cfg::SMEM_BYTES, st, 1, ta, tb, tc, p);
+  const int units = (int)((int64_t)(p.num_tiles / p.num_n_tiles) * ((p.num_n_tiles + CL / 2 - 1) / (CL / 2)));
+  // co-resident clusters: GPC boundaries can leave fewer than SMs / CL slots
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * (g_num_sms / CL));
+    cfg.blockDim = dim3(Cfg::NUM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, zq_gemm2_kernel<BN, KIND, CL>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = g_num_sms / CL;
+    }
+    max_clusters = n < g_num_sms / CL ? n : g_num_sms / CL;
+    if (getenv("ZQ_GEMM_DEBUG")) fprintf(stderr, "[zq] gemm2 BN=%d CL=%d: %d co-resident clusters\n", BN, CL, max_clusters);
+  }
+  const int clusters = units < max_clusters ? units : max_clusters;
+  const cudaError_t e = launch_kernel(zq_gemm2_kernel<BN, KIND, CL>, dim3(CL * clusters), dim3(Cfg::NUM_THREADS),
+                                      Cfg::SMEM_BYTES, st, CL, ta, tb, tc, p);
   if (e != cudaSuccess) {
     set_error("tcgen05 cta-pair gemm launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
@@ -1573,7 +1623,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   }
   if (w_bits == 8 && pair_mode != 0) {
     const int64_t mp = (M + 2 * BLOCK_M - 1) / (2 * BLOCK_M);
-    int bn2 = 0;
+    int bn2 = 0, cl2 = 2;
     static int force_bn2 = -1;
     if (force_bn2 < 0) {
       const char* e = getenv("ZQ_GEMM_BN2");
@@ -1587,19 +1637,37 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       double best = 1e30;
       for (int cand : {256, 192, 128}) {
         if (cand > N && cand > 128) continue;
-        const double tiles = (double)mp * (double)((N + cand - 1) / cand);
-        const double rounds = std::ceil(tiles / (g_num_sms / 2));
-        const double t_mma = 128.0 * cand * K / 11.1e12;
-        const double t_op = (128.0 + cand / 2) * K / 75e9;
-        const double t_epi = 128.0 * cand * esz / 35e9;
-        const double t = rounds * std::max(t_mma, std::max(t_op, t_epi)) + t_op;
-        if (t < best * 0.97) {  // prefer the wider tile unless the narrower one is clearly faster
-          best = t;
-          bn2 = cand;
+        // CL = 4 (A multicast across two pairs) only when forced: clusters of 4 fit
+        // 33 per GPU (GPC boundaries) against 74 pairs, and the ~5% per-SM gain
+        // does not repay the 11% of SMs left idle (8192^3: 373 vs 350 us)
+        for (int cl : {2}) {
+          const int64_t nt = (N + cand - 1) / cand;
+          if (cl == 4 && nt < 2) continue;
+          const double units = (double)mp * (double)((nt + cl / 2 - 1) / (cl / 2));
+          const double rounds = std::ceil(units / (g_num_sms / cl));
+          const double t_mma = 128.0 * cand * K / 11.1e12;
+          // operand delivery: the L2 -> SM rate (~75 GB/s per SM); with CL = 4 each
+          // CTA pulls half of its A tile (the other half arrives by multicast)
+          const double t_op = (128.0 / (cl / 2) + cand / 2) * K / 75e9;
+          const double t_epi = 128.0 * cand * esz / 35e9;
+          const double t = rounds * std::max(t_mma, std::max(t_op, t_epi)) + t_op;
+          if (t < best * 0.97) {  // prefer the earlier (wider / simpler) choice unless clearly faster
+            best = t;
+            bn2 = cand;
+            cl2 = cl;
+          }
         }
       }
     }
     if (force_bn2 && bn2) bn2 = force_bn2;
+    {
+      static int force_cl = -1;
+      if (force_cl < 0) {
+        const char* e = getenv("ZQ_GEMM_CL");
+        force_cl = e ? atoi(e) : 0;
+      }
+      if (bn2 && (force_cl == 2 || (force_cl == 4 && (N + bn2 - 1) / bn2 >= 2))) cl2 = force_cl;
+    }
     if (bn2) {
       CUtensorMap ta, tb;
       int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1635,9 +1703,10 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.num_tiles = (int)mp * p.num_n_tiles;
       p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
       p.group_m = K >= 2048 ? 8 : 1;  // operand-bound: keep A / B panels in L2
-#define ZQ_G2(KK) (bn2 == 256 ? launch_gemm2_t<256, KK>(ta, tb, tc, p, st) \
-                   : bn2 == 192 ? launch_gemm2_t<192, KK>(ta, tb, tc, p, st)  \
-                                : launch_gemm2_t<128, KK>(ta, tb, tc, p, st))
+#define ZQ_G2C(KK, CC) (bn2 == 256 ? launch_gemm2_t<256, KK, CC>(ta, tb, tc, p, st) \
+                        : bn2 == 192 ? launch_gemm2_t<192, KK, CC>(ta, tb, tc, p, st)  \
+                                     : launch_gemm2_t<128, KK, CC>(ta, tb, tc, p, st))
+#define ZQ_G2(KK) (cl2 == 4 ? ZQ_G2C(KK, 4) : ZQ_G2C(KK, 2))
       switch (kind) {
         case OUT_S32: return ZQ_G2(OUT_S32);
         case OUT_F32: return ZQ_G2(OUT_F32);
