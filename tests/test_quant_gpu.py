@@ -257,6 +257,17 @@ def test_gelu_quantize_fast_path_exact(zq, std):
         assert same_bits(h(qa.values), q_ref), (t, d, std)
 
 
+def test_gelu_quantize_wide_rows(zq):
+    """Rows wider than 8 chunks x 128 threads with too many rows for a cluster split
+    (NeoX FFN prefill: 24576 columns, one CTA of 768 threads per row)."""
+    _, igemm = zq
+    x = (np.random.default_rng(41).standard_normal((320, 24576)) * 1.5).astype(F32)
+    qa = igemm.gelu_quantize(x, 8)
+    q_ref, s_ref = O.gelu_quantize(x, 8)
+    assert same_bits(h(qa.token_scales), s_ref)
+    assert same_bits(h(qa.values), q_ref)
+
+
 def test_ln_uniform_and_generic_paths_agree(zq):
     """Balanced-tree (uniform) and generic plan LN kernels vs numpy for widths
     around the uniform/non-uniform boundary."""
