@@ -303,36 +303,47 @@ __global__ void __launch_bounds__(256, 1)
         s[32 + j] = __uint_as_float(r1[j]);
       }
     }
+    // scores * inv (transformer.py:432) is folded into the exponent: the max is
+    // taken over raw scores (inv > 0) and exp(inv (s - max)) = 2^(s c - max c),
+    // c = inv log2(e); the common rounding of max c cancels in the normalisation
     float mx = -INFINITY;
+    if (seq == kAttT && !causal) {  // no masked keys (BERT's full 128-token rows)
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const int key = half * 64 + j;
-      float v = __fmul_rn(s[j], scale);                        // scores *= inv (transformer.py:432)
-      if (key >= seq || (causal && key > row)) v = -INFINITY;  // mask (transformer.py:433-434)
-      s[j] = v;
-      mx = fmaxf(mx, v);
+      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = half * 64 + j;
+        if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
+        mx = fmaxf(mx, s[j]);
+      }
     }
     red[half * 128 + row] = mx;
     __syncthreads();
     mx = fmaxf(red[row], red[128 + row]);
-    // exp(s - mx) = 2^((s - mx) * log2 e), branch-free: masked scores give 2^-inf = 0
-    float sum = 0.0f;
+    const float c = __fmul_rn(scale, 1.4426950408889634f);
+    const float mxc = __fmul_rn(mx, c);
+    // branch-free: masked scores give 2^-inf = 0; four partial sums for ILP
+    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int j = 0; j < 64; ++j) {
-      const float e = ex2_approx_f(__fmul_rn(__fsub_rn(s[j], mx), 1.4426950408889634f));
+      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
       s[j] = e;
-      sum = __fadd_rn(sum, e);
+      sp[j & 3] = __fadd_rn(sp[j & 3], e);
     }
+    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
     __syncthreads();
     red[half * 128 + row] = sum;
     __syncthreads();
     sum = __fadd_rn(red[row], red[128 + row]);
+    // P is left unnormalised (entries in [0, 1]); the 1 / sum is applied to the
+    // 64 outputs of the row instead of its 128 probabilities
     const float inv_sum = __frcp_rn(sum);
 #pragma unroll
     for (int c2 = 0; c2 < 2; ++c2) {
       float hi[32], lo[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) split_tf32(__fmul_rn(s[32 * c2 + j], inv_sum), hi[j], lo[j]);
+      for (int j = 0; j < 32; ++j) split_tf32(s[32 * c2 + j], hi[j], lo[j]);
       const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + half * 64 + 32 * c2;
       tmem_st_32x32b_x32(ta, hi);
       tmem_st_32x32b_x32(ta + 128, lo);
@@ -365,6 +376,8 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t r0[32];
       tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16) + 256 + half * 32, r0);
       tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), inv_sum));
       if (tma_store) {
         // stage O in lo(K) (dead after S) as two [128 rows x 32 cols] SWIZZLE_128B
         // boxes; one bulk tensor store per box drains while the next head runs
