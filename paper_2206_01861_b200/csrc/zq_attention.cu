@@ -43,6 +43,7 @@ constexpr int kAttD = 64;    // head dim
 // of P.V (64 rows = head dim, 4 atoms of 32 tokens).  P hi / lo (128 x 128 f32,
 // 4 K-major atoms each) overlay Qh..Kl once S is computed.
 constexpr int kRegion = kAttT * kAttD * 4;         // 32 KB
+constexpr uint32_t kTmemQ = 320;                   // TMEM columns of Q hi [320,384) / lo [384,448)
 constexpr int kAttSmem = 7 * kRegion + 64 + 2 * 128 * 4;  // + barriers / TMEM slot / row partials
 
 __device__ __forceinline__ uint32_t make_idesc_tf32(int M, int N, int b_mn_major) {
@@ -227,16 +228,32 @@ __global__ void __launch_bounds__(256, 1)
       __syncthreads();
     }
     if (tr && it < 8) tr[it * 8 + 1] = gtime();
-    // ---- lo(Q), lo(K) in place; V -> K-major V^T hi / lo ----
-    for (int i = tid; i < 2 * (kRegion / 16); i += 256) {
-      const int part = i / (kRegion / 16), off = (i % (kRegion / 16)) * 16;
-      const float4 x = *reinterpret_cast<const float4*>(sm + 2 * part * kRegion + off);
+    // ---- Q -> TMEM as hi / lo (the S MMAs read A from TMEM: Q leaves smem once);
+    //      lo(K) in place; V -> K-major V^T hi / lo ----
+    {
+      const uint8_t* qrow = sQh + half * (kRegion / 2) + row * 128;
+      float qh[32], ql[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 x = *reinterpret_cast<const float4*>(qrow + ((c ^ (row & 7)) << 4));
+        split_tf32(x.x, qh[4 * c], ql[4 * c]);
+        split_tf32(x.y, qh[4 * c + 1], ql[4 * c + 1]);
+        split_tf32(x.z, qh[4 * c + 2], ql[4 * c + 2]);
+        split_tf32(x.w, qh[4 * c + 3], ql[4 * c + 3]);
+      }
+      const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + kTmemQ + half * 32;
+      tmem_st_32x32b_x32(tq, qh);
+      tmem_st_32x32b_x32(tq + kAttD, ql);
+    }
+    for (int i = tid; i < kRegion / 16; i += 256) {
+      const int off = i * 16;
+      const float4 x = *reinterpret_cast<const float4*>(sKh + off);
       float4 hi, lo;
       split_tf32(x.x, hi.x, lo.x);
       split_tf32(x.y, hi.y, lo.y);
       split_tf32(x.z, hi.z, lo.z);
       split_tf32(x.w, hi.w, lo.w);
-      *reinterpret_cast<float4*>(sm + (2 * part + 1) * kRegion + off) = lo;
+      *reinterpret_cast<float4*>(sKl + off) = lo;
     }
     {
       const int j = (warp & 1) * 32 + lane;  // head-dim column
@@ -261,6 +278,7 @@ __global__ void __launch_bounds__(256, 1)
         *reinterpret_cast<float4*>(sVl + o) = lo;
       }
     }
+    tmem_st_wait();
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -271,16 +289,15 @@ __global__ void __launch_bounds__(256, 1)
     // ---- S = Q K^T (3-term split) -> TMEM [0,128) ----
     if (warp == 0) {
       const uint32_t idesc = make_idesc_tf32(128, 128, 0);
-      const uint64_t dQh = make_sw128_desc(smem_u32(sQh)), dQl = make_sw128_desc(smem_u32(sQl));
       const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
 #pragma unroll
       for (int t3 = 0; t3 < 3; ++t3)
 #pragma unroll
         for (int ks = 0; ks < kAttD / 8; ++ks) {
           const int kb = 32 * ks;
-          const uint64_t aoff = (uint64_t)(((kb >> 7) * kAttT * 128 + (kb & 127)) >> 4);
-          mma_tf32_elect(tmem, (t3 == 2 ? dQl : dQh) + aoff, (t3 == 1 ? dKl : dKh) + aoff, idesc,
-                         (t3 | ks) != 0);
+          const uint64_t boff = (uint64_t)(((kb >> 7) * kAttT * 128 + (kb & 127)) >> 4);
+          mma_tf32_ts_elect(tmem, tmem + kTmemQ + (t3 == 2 ? kAttD : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + boff,
+                            idesc, (t3 | ks) != 0);
         }
       mma_commit_elect(&bar[2]);
     }
