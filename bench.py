@@ -216,78 +216,95 @@ def build_engine(torch, seed_base: int = 0, lanes: int | None = None):
 
 
 def gemm_roofline(torch, eng, peaks, basis):
-    """Time every fused W8A8 linear of one eager forward with CUDA events on the
-    launching stream.  Each launch is bounded by max(ops / P_int8, bytes / B_hbm)
-    (SURVEY.md §8d); at BERT-base shapes the f32 outputs make three of the four
-    GEMMs HBM-bound, so the line reports algorithmic bytes / summed launch time
-    against the HBM peak, with the tensor-side rate and the per-launch roofline
-    fraction alongside."""
-    events = []
-    engines = eng._sub or [eng]  # lanes run one after another here: per-launch times
+    """Per-launch time of the fused W8A8 linears of one forward: the calls are
+    recorded from an eager forward, replayed back to back in a CUDA graph (the
+    same buffers, so the same work) and timed with CUDA events on the replay
+    stream — no host launch gaps or per-call event overhead in the figure.  Each
+    launch is bounded by max(ops / P_int8, bytes / B_hbm); at
+    BERT-base shapes the f32 outputs make three of the four GEMMs HBM-bound, so
+    the line reports algorithmic bytes / launch time against the HBM peak, with
+    the tensor-side rate and the per-launch roofline fraction alongside."""
+    calls = []
+    engines = eng._sub or [eng]
     origs = [e._linear for e in engines]
 
-    def make_timed(orig):
-        def timed_linear(q, s, w, bias, out):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
+    def make_rec(orig):
+        def rec(q, s, w, bias, out):
             orig(q, s, w, bias, out)
-            b.record()
-            m, k = q.shape
-            n = w.rows
-            nbytes = m * k + n * k * w.bits // 8 + m * n * out.element_size() + 4 * m + 8 * n
-            events.append((a, b, 2 * m * k * n, nbytes))
-        return timed_linear
+            calls.append((orig, (q, s, w, bias, out)))
+        return rec
 
     origs_ln = [e._linear_ln for e in engines]
 
-    def make_timed_ln(orig):
-        def timed(q, s, w, bias, res, g, b, ln_out, qo, so, ws):
-            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            ok = orig(q, s, w, bias, res, g, b, ln_out, qo, so, ws)
-            b2.record()
-            if ok:  # GEMM + residual read + LN out f32 + int8 + scales
-                m, k = q.shape
-                n = w.rows
-                nbytes = m * k + n * k + 4 * m * n + 4 * m * n + m * n + 8 * m + 16 * n
-                events.append((a, b2, 2 * m * k * n, nbytes))
+    def make_rec_ln(orig):
+        def rec(*a):
+            ok = orig(*a)
+            if ok:
+                calls.append((orig, a))
             return ok
-        return timed
+        return rec
 
     for e, o, ol in zip(engines, origs, origs_ln):
-        e._linear = make_timed(o)
-        e._linear_ln = make_timed_ln(ol)
+        e._linear = make_rec(o)
+        e._linear_ln = make_rec_ln(ol)
     try:
-        for _ in range(3):
-            events.clear()
-            for e in engines:
-                e._run()
+        for e in engines:
+            e._run()
         torch.cuda.synchronize()
     finally:
         for e, o, ol in zip(engines, origs, origs_ln):
             e._linear = o
             e._linear_ln = ol
-    times = [a.elapsed_time(b) * 1e-3 for a, b, _, _ in events]
-    t = sum(times)
-    ops = sum(o for _, _, o, _ in events)
-    nbytes = sum(nb for _, _, _, nb in events)
+    ops_l, bytes_l = [], []
+    for f, a in calls:
+        q, w = a[0], a[2]
+        m, k = q.shape
+        n = w.rows
+        if len(a) == 5:
+            out = a[4]
+            nb = m * k + n * k * w.bits // 8 + m * n * out.element_size() + 4 * m + 8 * n
+        else:  # GEMM + residual read + LN out f32 + int8 + scales
+            nb = m * k + n * k + 4 * m * n + 4 * m * n + m * n + 8 * m + 16 * n
+        ops_l.append(2 * m * k * n)
+        bytes_l.append(nb)
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for f, a in calls:
+            f(*a)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for f, a in calls:
+                f(*a)
+        g.replay()
+        st.synchronize()
+        reps = 10
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for _ in range(reps):
+            g.replay()
+        t1.record(st)
+        t1.synchronize()
+    t_per_pass = t0.elapsed_time(t1) * 1e-3 / reps
+    n_l = max(1, len(calls))
+    ops, nbytes = sum(ops_l), sum(bytes_l)
     p_int8 = 2.0 * peaks["bf16_tflops"] * 1e12
     p_hbm = peaks["hbm_gbs"] * 1e9
-    t_roof = sum(max(o / p_int8, nb / p_hbm) for _, _, o, nb in events)
+    t_roof = sum(max(o / p_int8, nb / p_hbm) for o, nb in zip(ops_l, bytes_l))
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("bert_gemm_bytes_per_launch")
-    achieved = nbytes / t / 1e9
+    achieved = nbytes / t_per_pass / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-            "kernel": "zq_gemm2_kernel / zq_gemm2_ln_kernel (W8A8 linear, tcgen05 kind::i8 CTA pairs; the O and "
-                      "4hh projections with residual + LayerNorm + quantize fused in)",
-            "launches_per_step": len(events), "per_launch_us": 1e6 * t / max(1, len(events)),
-            "algorithmic_bytes_per_launch": nbytes / max(1, len(events)),
-            "tensor_tflops": ops / t / 1e12, "tensor_peak": p_int8 / 1e12,
-            "frac_of_per_launch_roofline": t_roof / t,
+            "kernel": "zq_gemm2_kernel (W8A8 linear, tcgen05 kind::i8 CTA pairs, dequant epilogue fused)",
+            "launches_per_step": n_l, "per_launch_us": 1e6 * t_per_pass / n_l,
+            "timing": "one forward's linears replayed back to back in a CUDA graph, CUDA events on the replay stream",
+            "algorithmic_bytes_per_launch": nbytes / n_l,
+            "tensor_tflops": ops / t_per_pass / 1e12, "tensor_peak": p_int8 / 1e12,
+            "frac_of_per_launch_roofline": t_roof / t_per_pass,
             "peak_basis": f"{basis} HBM copy bandwidth; int8 peak = 2 x {basis} bf16 dense "
                           f"({peaks['bf16_tflops']} TF/s): kind::i8 issues at twice the kind::f16 rate"}
 
