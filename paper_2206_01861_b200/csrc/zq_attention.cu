@@ -29,6 +29,7 @@
 //      (M=128, N=64, K=128) -> TMEM cols [256,320);
 //   6. 8 warps read O and store ctx rows (f32).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <string.h>
 
 #include "zq_common.cuh"
@@ -429,6 +430,352 @@ __global__ void __launch_bounds__(256, 1)
 
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// fp16 two-term variant (default for seq <= 128).  Every operand tile is scaled
+// by a power of two so its max lands in [2^14, 2^15) and split as
+// hi = f16(x'), lo = f16(x' - hi) (22 significant bits; products hi*hi + hi*lo +
+// lo*hi, relative error ~2^-21 like the 3xTF32 kernel), and the six MMAs run as
+// tcgen05 kind::f16 — twice the kind::tf32 rate, with half the shared-memory
+// bytes per operand.  P (in [0, 1]) is scaled by 2^15.  The scales are exact
+// powers of two, folded into the softmax exponent (S) and the output (O).
+//   smem: raw Q | raw K | raw V (TMA, f32) | K hi | K lo (f16, K-major SW128) |
+//         V^T hi | V^T lo (f16, 2 atoms of [64 x 128 B]) | O staging (f32)
+//   TMEM (256 cols): S [0,128) -> P hi [0,64) / P lo [64,128) (f16x2), O [128,192),
+//         Q hi [192,224), Q lo [224,256) (f16x2)
+// The raw Q / K / V tiles are consumed by the split, so the next head's loads go
+// out before this head's first MMA.
+// ---------------------------------------------------------------------------
+constexpr int kH16 = 128 * 64 * 2;                    // one f16 operand tile: 16 KB
+constexpr int kAtt16Smem = 3 * kRegion + 4 * kH16 + kRegion + 64 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr uint32_t kT16O = 128, kT16Q = 192;
+
+__device__ __forceinline__ uint32_t make_idesc_f16(int M, int N) {
+  return (1u << 4)  // c_format F32; a_format = b_format = F16 (0); both K-major
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// x -> (hi, lo) f16 halves of the pair (a, b) packed low = a, high = b
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(__fsub_rn(a, hf.x), __fsub_rn(b, hf.y));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// power-of-two factor f with max * f in [2^14, 2^15) (clamped to normal range)
+__device__ __forceinline__ float pow2_scale_for(uint32_t max_bits) {
+  const int E = (int)((max_bits >> 23) & 0xFF);
+  int F = 268 - E;
+  F = F < 1 ? 1 : (F > 254 ? 254 : F);
+  return __uint_as_float((uint32_t)F << 23);
+}
+__device__ __forceinline__ float pow2_inv(float f) {  // exact 1/f for a power of two
+  return __uint_as_float((uint32_t)(254 - (int)(__float_as_uint(f) >> 23)) << 23);
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x32u(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1)
+    attention_f16_kernel(const __grid_constant__ CUtensorMap tm, int seq, int heads, int dmodel, int causal,
+                         float scale, float* __restrict__ ctx, int64_t ld_ctx, int nheads_total,
+                         unsigned long long* __restrict__ trace, const __grid_constant__ CUtensorMap tmc,
+                         int tma_store) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + kRegion;
+  uint8_t* sV = sm + 2 * kRegion;
+  uint8_t* sKh = sm + 3 * kRegion;
+  uint8_t* sKl = sKh + kH16;
+  uint8_t* sVh = sKl + kH16;
+  uint8_t* sVl = sVh + kH16;
+  uint8_t* sO = sVl + kH16;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + kRegion);  // QK, V, S, O
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bar + 5);     // [8 warps][3]
+  float* red = reinterpret_cast<float*>(rmax + 24);          // [2][128] row partials
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    prefetch_tmap(&tm);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+
+  auto issue_all = [&](int hd) {
+    const int b = hd / heads, h = hd % heads;
+    mbar_arrive_expect_tx(&bar[0], 6 * 128 * 128);  // 3 tiles x 2 boxes x 16 KB
+#pragma unroll
+    for (int part = 0; part < 3; ++part)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        tma_load_2d(sm + part * kRegion + j * (kRegion / 2), &tm, &bar[0], part * dmodel + h * kAttD + 32 * j,
+                    b * seq);
+  };
+
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0 && (int)blockIdx.x < nheads_total) issue_all(blockIdx.x);
+  int it = 0;
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
+  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+    const uint32_t ph = it & 1;
+    if (tr && it < 8) tr[it * 8 + 0] = gtime();
+    const int nxt = hd + gridDim.x;
+    const int b = hd / heads, h = hd % heads;
+    mbar_wait(&bar[0], ph);
+    if (tr && it < 8) tr[it * 8 + 1] = gtime();
+
+    // ---- raw tiles -> registers: Q / K row halves (row, 32 dims), V^T (dim d, 32 tokens) ----
+    float q[32], k[32], v[32];
+    {
+      const uint8_t* qr = sQ + half * (kRegion / 2) + row * 128;
+      const uint8_t* kr = sK + half * (kRegion / 2) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 a = *reinterpret_cast<const float4*>(qr + ((c ^ (row & 7)) << 4));
+        const float4 bb = *reinterpret_cast<const float4*>(kr + ((c ^ (row & 7)) << 4));
+        q[4 * c] = a.x, q[4 * c + 1] = a.y, q[4 * c + 2] = a.z, q[4 * c + 3] = a.w;
+        k[4 * c] = bb.x, k[4 * c + 1] = bb.y, k[4 * c + 2] = bb.z, k[4 * c + 3] = bb.w;
+      }
+    }
+    const int vd = tid & 63, vtb = tid >> 6;  // V^T row (head dim) and 32-token block
+    {
+      const uint8_t* vc = sV + (vd >> 5) * (kRegion / 2) + (vd & 3) * 4;
+      const int jc = (vd & 31) >> 2;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int t = 32 * vtb + i;
+        v[i] = *reinterpret_cast<const float*>(vc + t * 128 + ((jc ^ (t & 7)) << 4));
+      }
+    }
+    uint32_t mq = 0, mk = 0, mv = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      mq = max(mq, __float_as_uint(q[i]) & 0x7fffffffu);
+      mk = max(mk, __float_as_uint(k[i]) & 0x7fffffffu);
+      mv = max(mv, __float_as_uint(v[i]) & 0x7fffffffu);
+    }
+    mq = __reduce_max_sync(0xffffffffu, mq);
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    mv = __reduce_max_sync(0xffffffffu, mv);
+    if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
+    __syncthreads();  // also: every thread's raw reads are done -> the next head may land
+    if (tid == 0 && nxt < nheads_total) issue_all(nxt);
+    {
+      uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
+               cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+      mq = __reduce_max_sync(0xffffffffu, a);
+      mk = __reduce_max_sync(0xffffffffu, bq);
+      mv = __reduce_max_sync(0xffffffffu, cq);
+    }
+    const float fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
+    // ---- Q -> TMEM hi / lo; K -> smem hi / lo; V^T -> smem hi / lo (f16) ----
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 16 * half, hi);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 32 + 16 * half, lo);
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = row * 128 + ((((4 * half + c) ^ (row & 7))) << 4);
+        *reinterpret_cast<uint4*>(sKh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sKl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(v[2 * j], fv), __fmul_rn(v[2 * j + 1], fv), hi[j], lo[j]);
+      const uint32_t atom = (uint32_t)(vtb >> 1) * (64 * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = atom + vd * 128 + ((((4 * (vtb & 1) + c) ^ (vd & 7))) << 4);
+        *reinterpret_cast<uint4*>(sVh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sVl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    tmem_st_wait();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 2] = gtime();
+
+    // ---- S' = Q' K'^T (f16 hi/lo, 3 terms) -> TMEM [0,128) ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, 128);
+      const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttD / 16; ++ks)
+          mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks, idesc,
+                           (t3 | ks) != 0);
+      mma_commit_elect(&bar[2]);
+    }
+    mbar_wait(&bar[2], ph);
+    tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 3] = gtime();
+
+    // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
+    float s[64];
+    {
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem + lane_base + half * 64;
+      tmem_ld_32x32b_x32(ta, r0);
+      tmem_ld_32x32b_x32(ta + 32, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        s[j] = __uint_as_float(r0[j]);
+        s[32 + j] = __uint_as_float(r1[j]);
+      }
+    }
+    float mx = -INFINITY;
+    if (seq == kAttT && !causal) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = half * 64 + j;
+        if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
+        mx = fmaxf(mx, s[j]);
+      }
+    }
+    red[half * 128 + row] = mx;
+    __syncthreads();
+    mx = fmaxf(red[row], red[128 + row]);
+    // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
+    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(fq)), pow2_inv(fk));
+    const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
+    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
+      s[j] = e;
+      sp[j & 3] = __fadd_rn(sp[j & 3], e);
+    }
+    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+    __syncthreads();
+    red[half * 128 + row] = sum;
+    __syncthreads();
+    sum = __fadd_rn(red[row], red[128 + row]);
+    // O = (P' V') / (fv sum'), sum' = 2^15 sum
+    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(fv));
+    {
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) split_f16x2(s[2 * j], s[2 * j + 1], hi[j], lo[j]);
+      tmem_st_32x32b_x32u(tmem + lane_base + 32 * half, hi);
+      tmem_st_32x32b_x32u(tmem + lane_base + 64 + 32 * half, lo);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 4] = gtime();
+
+    // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T (2 atoms along keys) ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, kAttD);
+      const uint64_t dVh = make_sw128_desc(smem_u32(sVh)), dVl = make_sw128_desc(smem_u32(sVl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttT / 16; ++ks) {
+          const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
+          mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                           (t3 | ks) != 0);
+        }
+      mma_commit_elect(&bar[3]);
+    }
+    mbar_wait(&bar[3], ph);
+    tc_fence_after();
+    if (tr && it < 8) tr[it * 8 + 5] = gtime();
+    {
+      uint32_t r0[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
+      if (tma_store) {
+        if (it > 0) {  // the previous head's O store must have read the staging buffer
+          if (tid == 0) bulk_wait_read0();
+          __syncthreads();
+        }
+        uint8_t* st = sO + half * (kRegion / 2) + row * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<uint4*>(st + ((cc ^ (row & 7)) << 4)) =
+              make_uint4(r0[4 * cc], r0[4 * cc + 1], r0[4 * cc + 2], r0[4 * cc + 3]);
+      } else if (row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
+                          __uint_as_float(r0[j + 3]));
+      }
+    }
+    if (tma_store) fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tma_store && tid == 0) {
+      tma_store_2d(&tmc, sO, h * kAttD, b * seq);
+      tma_store_2d(&tmc, sO + kRegion / 2, h * kAttD + 32, b * seq);
+      bulk_commit();
+    }
+    if (tr && it < 8) tr[it * 8 + 6] = gtime();
+  }
+  if (tma_store && tid == 0) bulk_wait0();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
 // Long sequences (seq > 128, head_dim 64): flash-attention style online softmax
 // over 128-key blocks.  Work item = (sequence, head, 128-query block), heaviest
 // causal blocks first; persistent CTAs.  TMEM: S [0,128), P hi [128,256),
@@ -745,6 +1092,7 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   if (!attr) {
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
+    cudaFuncSetAttribute(attention_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAtt16Smem);
     attr = true;
   }
   int nsm = 148;
@@ -765,9 +1113,19 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
                                 CU_TENSOR_MAP_SWIZZLE_128B) == ZQ_OK;
     }
     if (!tma_store) memset(&tmc, 0, sizeof(tmc));
-    e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem, reinterpret_cast<cudaStream_t>(stream),
-                      1, tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
-                      tma_store);
+    static int use_tf32 = -1;
+    if (use_tf32 < 0) {
+      const char* ev = getenv("ZQ_ATT_TF32");
+      use_tf32 = ev ? atoi(ev) : 0;
+    }
+    if (use_tf32)
+      e = launch_kernel(attention_kernel, dim3(grid), dim3(256), kAttSmem, reinterpret_cast<cudaStream_t>(stream),
+                        1, tm, seq, heads, heads * head_dim, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
+                        tma_store);
+    else
+      e = launch_kernel(attention_f16_kernel, dim3(grid), dim3(256), kAtt16Smem,
+                        reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads, heads * head_dim, causal, scale,
+                        ctx, ld_ctx, total, g_att_trace, tmc, tma_store);
   } else {
     const int nq = (seq + kAttT - 1) / kAttT;
     const int items = total * nq;
