@@ -439,14 +439,16 @@ __global__ void __launch_bounds__(256, 1)
 // bytes per operand.  P (in [0, 1]) is scaled by 2^15.  The scales are exact
 // powers of two, folded into the softmax exponent (S) and the output (O).
 //   smem: raw Q | raw K | raw V (TMA, f32) | K hi | K lo (f16, K-major SW128) |
-//         V^T hi | V^T lo (f16, 2 atoms of [64 x 128 B]) | O staging (f32)
+//         2 x (V^T hi | V^T lo) (f16, 2 atoms of [64 x 128 B]) | O staging (f32)
 //   TMEM (256 cols): S [0,128) -> P hi [0,64) / P lo [64,128) (f16x2), O [128,192),
 //         Q hi [192,224), Q lo [224,256) (f16x2)
-// The raw Q / K / V tiles are consumed by the split, so the next head's loads go
-// out before this head's first MMA.
+// Software pipeline per CTA: split(h+1) (CUDA cores, smem) runs while the tensor
+// core computes P V of head h (V^T double-buffered), and S(h+1) is issued before
+// O(h) is read out.  The raw tiles are consumed by the split, so the loads of
+// head h+2 go out during split(h+1).
 // ---------------------------------------------------------------------------
 constexpr int kH16 = 128 * 64 * 2;                    // one f16 operand tile: 16 KB
-constexpr int kAtt16Smem = 3 * kRegion + 4 * kH16 + kRegion + 64 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr int kAtt16Smem = 3 * kRegion + 6 * kH16 + kRegion + 64 + 3 * 8 * 4 + 2 * 128 * 4;
 constexpr uint32_t kT16O = 128, kT16Q = 192;
 
 __device__ __forceinline__ uint32_t make_idesc_f16(int M, int N) {
@@ -514,10 +516,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sV = sm + 2 * kRegion;
   uint8_t* sKh = sm + 3 * kRegion;
   uint8_t* sKl = sKh + kH16;
-  uint8_t* sVh = sKl + kH16;
-  uint8_t* sVl = sVh + kH16;
-  uint8_t* sO = sVl + kH16;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + kRegion);  // QK, V, S, O
+  uint8_t* sVT = sKl + kH16;  // [2 buffers][hi | lo]
+  uint8_t* sO = sVT + 4 * kH16;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + kRegion);  // raw, -, S, O
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
   uint32_t* rmax = reinterpret_cast<uint32_t*>(bar + 5);     // [8 warps][3]
   float* red = reinterpret_cast<float*>(rmax + 24);          // [2][128] row partials
@@ -538,7 +539,7 @@ __global__ void __launch_bounds__(256, 1)
   const int row = quarter * 32 + lane;
   const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
 
-  auto issue_all = [&](int hd) {
+  auto issue_raw = [&](int hd) {
     const int b = hd / heads, h = hd % heads;
     mbar_arrive_expect_tx(&bar[0], 6 * 128 * 128);  // 3 tiles x 2 boxes x 16 KB
 #pragma unroll
@@ -549,20 +550,10 @@ __global__ void __launch_bounds__(256, 1)
                     b * seq);
   };
 
-  pdl_trigger();
-  pdl_wait();
-  if (tid == 0 && (int)blockIdx.x < nheads_total) issue_all(blockIdx.x);
-  int it = 0;
-  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
-  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
-    const uint32_t ph = it & 1;
-    if (tr && it < 8) tr[it * 8 + 0] = gtime();
-    const int nxt = hd + gridDim.x;
-    const int b = hd / heads, h = hd % heads;
-    mbar_wait(&bar[0], ph);
-    if (tr && it < 8) tr[it * 8 + 1] = gtime();
-
-    // ---- raw tiles -> registers: Q / K row halves (row, 32 dims), V^T (dim d, 32 tokens) ----
+  // raw tiles of head hd (landed) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo (buffer vb)
+  // in smem; returns the head's three power-of-two scales.  Issues the raw loads
+  // of head hd_after as soon as every thread has read the raw tiles.
+  auto split = [&](int hd_after, int vb, float& fq, float& fk, float& fv) {
     float q[32], k[32], v[32];
     {
       const uint8_t* qr = sQ + half * (kRegion / 2) + row * 128;
@@ -595,18 +586,18 @@ __global__ void __launch_bounds__(256, 1)
     mq = __reduce_max_sync(0xffffffffu, mq);
     mk = __reduce_max_sync(0xffffffffu, mk);
     mv = __reduce_max_sync(0xffffffffu, mv);
+    __syncthreads();  // rmax of the previous split has been read by everyone
     if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
     __syncthreads();  // also: every thread's raw reads are done -> the next head may land
-    if (tid == 0 && nxt < nheads_total) issue_all(nxt);
+    if (tid == 0 && hd_after < nheads_total) issue_raw(hd_after);
     {
-      uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
-               cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+      const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
+                     cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
       mq = __reduce_max_sync(0xffffffffu, a);
       mk = __reduce_max_sync(0xffffffffu, bq);
       mv = __reduce_max_sync(0xffffffffu, cq);
     }
-    const float fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
-    // ---- Q -> TMEM hi / lo; K -> smem hi / lo; V^T -> smem hi / lo (f16) ----
+    fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
     {
       uint32_t hi[16], lo[16];
 #pragma unroll
@@ -629,12 +620,14 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t hi[16], lo[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(v[2 * j], fv), __fmul_rn(v[2 * j + 1], fv), hi[j], lo[j]);
+      uint8_t* vh = sVT + vb * (2 * kH16);
+      uint8_t* vl = vh + kH16;
       const uint32_t atom = (uint32_t)(vtb >> 1) * (64 * 128);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t off = atom + vd * 128 + ((((4 * (vtb & 1) + c) ^ (vd & 7))) << 4);
-        *reinterpret_cast<uint4*>(sVh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-        *reinterpret_cast<uint4*>(sVl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+        *reinterpret_cast<uint4*>(vh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(vl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
       }
     }
     tmem_st_wait();
@@ -642,9 +635,8 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (tr && it < 8) tr[it * 8 + 2] = gtime();
-
-    // ---- S' = Q' K'^T (f16 hi/lo, 3 terms) -> TMEM [0,128) ----
+  };
+  auto issue_s = [&]() {
     if (warp == 0) {
       const uint32_t idesc = make_idesc_f16(128, 128);
       const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
@@ -656,9 +648,29 @@ __global__ void __launch_bounds__(256, 1)
                            (t3 | ks) != 0);
       mma_commit_elect(&bar[2]);
     }
+  };
+
+  pdl_trigger();
+  pdl_wait();
+  // prologue: first head's split and S
+  float fq = 1.0f, fk = 1.0f, fv = 1.0f;
+  if ((int)blockIdx.x < nheads_total) {
+    if (tid == 0) issue_raw(blockIdx.x);
+    mbar_wait(&bar[0], 0);
+    split((int)blockIdx.x + (int)gridDim.x, 0, fq, fk, fv);
+    issue_s();
+  }
+  int it = 0;
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
+  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+    const uint32_t ph = it & 1;
+    if (tr && it < 8) tr[it * 8 + 0] = gtime();
+    const int nxt = hd + gridDim.x;
+    const int b = hd / heads, h = hd % heads;
+    const float cfq = fq, cfk = fk, cfv = fv;  // this head's scales (split(nxt) overwrites)
     mbar_wait(&bar[2], ph);
     tc_fence_after();
-    if (tr && it < 8) tr[it * 8 + 3] = gtime();
+    if (tr && it < 8) tr[it * 8 + 1] = gtime();
 
     // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
     float s[64];
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     mx = fmaxf(red[row], red[128 + row]);
     // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
-    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(fq)), pow2_inv(fk));
+    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
     const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
     float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -705,7 +717,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     sum = __fadd_rn(red[row], red[128 + row]);
     // O = (P' V') / (fv sum'), sum' = 2^15 sum
-    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(fv));
+    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
     {
       uint32_t hi[32], lo[32];
 #pragma unroll
@@ -717,12 +729,13 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (tr && it < 8) tr[it * 8 + 4] = gtime();
+    if (tr && it < 8) tr[it * 8 + 2] = gtime();
 
-    // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T (2 atoms along keys) ----
+    // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T buffer it & 1 ----
     if (warp == 0) {
       const uint32_t idesc = make_idesc_f16(128, kAttD);
-      const uint64_t dVh = make_sw128_desc(smem_u32(sVh)), dVl = make_sw128_desc(smem_u32(sVl));
+      const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
+      const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
 #pragma unroll
       for (int t3 = 0; t3 < 3; ++t3)
 #pragma unroll
@@ -733,9 +746,16 @@ __global__ void __launch_bounds__(256, 1)
         }
       mma_commit_elect(&bar[3]);
     }
+    // ---- the next head's split runs while the tensor core computes P V ----
+    if (nxt < nheads_total) {
+      mbar_wait(&bar[0], (it + 1) & 1);
+      split(nxt + (int)gridDim.x, (it + 1) & 1, fq, fk, fv);
+    }
+    if (tr && it < 8) tr[it * 8 + 3] = gtime();
     mbar_wait(&bar[3], ph);
     tc_fence_after();
-    if (tr && it < 8) tr[it * 8 + 5] = gtime();
+    if (nxt < nheads_total) issue_s();  // P of this head is consumed: S of the next may overwrite it
+    if (tr && it < 8) tr[it * 8 + 4] = gtime();
     {
       uint32_t r0[32];
       tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
@@ -770,7 +790,7 @@ __global__ void __launch_bounds__(256, 1)
       tma_store_2d(&tmc, sO + kRegion / 2, h * kAttD + 32, b * seq);
       bulk_commit();
     }
-    if (tr && it < 8) tr[it * 8 + 6] = gtime();
+    if (tr && it < 8) tr[it * 8 + 5] = gtime(), tr[it * 8 + 6] = gtime();
   }
   if (tma_store && tid == 0) bulk_wait0();
   if (warp == 0) tmem_dealloc(tmem, 256);
