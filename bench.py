@@ -547,6 +547,35 @@ def run_gpt(args, rank: int, world: int, dist):
         e2e.append((a, b))
     barrier()
     e2e_s = sum(x.elapsed_time(y) for x, y in e2e) * 1e-3
+    # our kernel launches per generation: count the C-ABI entry points one eager
+    # prefill and one eager decode step make (each launches one kernel; the LM
+    # head's cuBLAS sgemm + argmax and the embedding gather are torch ops, not ours).
+    # decoder.attention wraps zq_attention_f32 and is counted there.
+    from paper_2206_01861_b200 import _native as N
+    from paper_2206_01861_b200 import transformer as T
+    calls = {"n": 0}
+    orig_call, orig_att = N.call, T.attention
+
+    def counting_call(name, *a):
+        calls["n"] += 1
+        return orig_call(name, *a)
+
+    def counting_att(*a, **kw):
+        calls["n"] += 1
+        return orig_att(*a, **kw)
+
+    from paper_2206_01861_b200 import decoder as D
+    N.call, D.attention = counting_call, counting_att
+    try:
+        eng.prefill(ids_dev)
+        n_prefill = calls["n"]
+        calls["n"] = 0
+        eng._step_launches()
+        n_step = calls["n"]
+    finally:
+        N.call, D.attention = orig_call, orig_att
+    torch.cuda.synchronize()
+    launches = args.steps * (n_prefill + (new - 1) * n_step)
     if dist is not None:
         t = torch.tensor([total, prefill_s, decode_s, e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -584,7 +613,8 @@ def run_gpt(args, rank: int, world: int, dist):
                      "kernel": "decode step: int8 weight streaming of all quantized linears (per rank)",
                      "peak_basis": f"{basis} HBM copy bandwidth (MEASURED_PEAKS.json)"},
         "cpu_baseline": {"value": cpu_val, "unit": "tok/s", "cores": cores, "kind": "port", "sample": cpu_sample},
-        "gpu_launches": None,
+        "gpu_launches": launches,
+        "gpu_launches_per": {"prefill": n_prefill, "decode_step": n_step},
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -796,6 +796,139 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
+// ---------------------------------------------------------------------------
+// Any head_dim (multiple of 32, <= 256) and any sequence length: CUDA-core fp32
+// flash attention (GPT-J 256 / NeoX 96 prefill).  A CTA takes 32 queries of one
+// (sequence, head): 4 warps x 8 query rows; per block of 32 keys lane l scores key
+// l against the warp's 8 rows with 16-byte loads (K rows padded by 4 floats:
+// conflict-free; Q rows are warp broadcasts), the
+// online softmax runs on warp shuffles, and P V accumulates into registers
+// (lane l owns head-dim columns l, l+32, ...), broadcasting p per key.  fp32 FMA
+// throughout (more accurate than the tensor-core paths; prefill only).
+// ---------------------------------------------------------------------------
+template <int DH>
+__global__ void __launch_bounds__(128)
+    attention_general_kernel(const float* __restrict__ qkv, int64_t ld_qkv, int seq, int heads, int causal,
+                             float scale, float* __restrict__ ctx, int64_t ld_ctx) {
+  constexpr int NJ = DH / 32;   // head-dim columns per lane
+  constexpr int RW = 8;         // query rows per warp
+  constexpr int QB = 4 * RW;    // query rows per CTA
+  constexpr int KP = DH + 4;    // padded K row (16-byte loads stay conflict-free)
+  extern __shared__ float4 smg4[];
+  float* sQ = reinterpret_cast<float*>(smg4);  // [QB][DH]
+  float* sK = sQ + QB * DH;                    // [32][KP]
+  float* sV = sK + 32 * KP;                    // [32][DH]
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = blockIdx.x * QB, h = blockIdx.y, b = blockIdx.z;
+  const int dmodel = heads * DH;
+  const float* base = qkv + (int64_t)b * seq * ld_qkv;
+  for (int i = threadIdx.x; i < QB * DH / 4; i += 128) {
+    const int r = i / (DH / 4), d4 = i - r * (DH / 4);
+    reinterpret_cast<float4*>(sQ)[i] =
+        q0 + r < seq ? *reinterpret_cast<const float4*>(base + (int64_t)(q0 + r) * ld_qkv + h * DH + 4 * d4)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float m[RW], l[RW], o[RW][NJ];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) o[r][j] = 0.0f;
+  }
+  const int qlast = min(seq, q0 + QB) - 1;
+  const int kend = causal ? qlast + 1 : seq;
+  const float c = __fmul_rn(scale, 1.4426950408889634f);
+  const float4* qrow = reinterpret_cast<const float4*>(sQ + warp * RW * DH);
+  for (int k0 = 0; k0 < kend; k0 += 32) {
+    __syncthreads();  // previous block's K / V fully consumed (and sQ written, first pass)
+    for (int i = threadIdx.x; i < 32 * DH / 4; i += 128) {
+      const int r = i / (DH / 4), d4 = i - r * (DH / 4);
+      const bool ok = k0 + r < seq;
+      const float* row = base + (int64_t)(k0 + r) * ld_qkv + h * DH + 4 * d4;
+      *reinterpret_cast<float4*>(sK + r * KP + 4 * d4) =
+          ok ? *reinterpret_cast<const float4*>(row + dmodel) : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(sV + r * DH + 4 * d4) =
+          ok ? *reinterpret_cast<const float4*>(row + 2 * dmodel) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    const int key = k0 + lane;
+    float sc[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) sc[r] = 0.0f;
+    const float4* krow = reinterpret_cast<const float4*>(sK + lane * KP);
+#pragma unroll 4
+    for (int d4 = 0; d4 < DH / 4; ++d4) {
+      const float4 kv = krow[d4];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        const float4 qv = qrow[r * (DH / 4) + d4];
+        sc[r] = __fmaf_rn(qv.x, kv.x, sc[r]);
+        sc[r] = __fmaf_rn(qv.y, kv.y, sc[r]);
+        sc[r] = __fmaf_rn(qv.z, kv.z, sc[r]);
+        sc[r] = __fmaf_rn(qv.w, kv.w, sc[r]);
+      }
+    }
+    float p[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int q = q0 + warp * RW + r;
+      const bool masked = key >= seq || (causal && key > q);
+      const float v = masked ? -INFINITY : sc[r];
+      float bm = v;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+      const float mn = fmaxf(m[r], bm);
+      // rows with every key so far masked keep m = -inf: nothing to rescale
+      const float corr = mn == -INFINITY ? 1.0f : ex2_approx_f(__fmul_rn(__fsub_rn(m[r], mn), c));
+      p[r] = mn == -INFINITY ? 0.0f : ex2_approx_f(__fmul_rn(__fsub_rn(v, mn), c));
+      float ps = p[r];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ps = __fadd_rn(ps, __shfl_xor_sync(0xffffffffu, ps, off));
+      l[r] = __fmaf_rn(l[r], corr, ps);
+      m[r] = mn;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) o[r][j] = __fmul_rn(o[r][j], corr);
+    }
+    const int nk = min(32, kend - k0);
+    for (int kk = 0; kk < nk; ++kk) {
+      float pk[RW];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) pk[r] = __shfl_sync(0xffffffffu, p[r], kk);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const float vv = sV[kk * DH + lane + 32 * j];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) o[r][j] = __fmaf_rn(pk[r], vv, o[r][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int q = q0 + warp * RW + r;
+    if (q >= seq) continue;
+    const float inv = __frcp_rn(l[r]);
+    float* dst = ctx + ((int64_t)b * seq + q) * ld_ctx + h * DH;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) dst[lane + 32 * j] = __fmul_rn(o[r][j], inv);
+  }
+}
+
+template <int DH>
+static cudaError_t launch_att_general(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads, int causal,
+                                      float scale, float* ctx, int64_t ld_ctx, cudaStream_t st) {
+  const size_t smem = sizeof(float) * (32 * DH + 32 * (DH + 4) + 32 * DH);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_general_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  return launch_kernel(attention_general_kernel<DH>, dim3((unsigned)((seq + 31) / 32), (unsigned)heads, (unsigned)batch),
+                       dim3(128), smem, st, 1, qkv, ld_qkv, seq, heads, causal, scale, ctx, ld_ctx);
+}
+
 // Long sequences (seq > 128, head_dim 64): flash-attention style online softmax
 // over 128-key blocks.  Work item = (sequence, head, 128-query block), heaviest
 // causal blocks first; persistent CTAs.  TMEM: S [0,128), P hi [128,256),
@@ -1100,7 +1233,29 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
                                 int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
                                 void* stream) {
   ZQ_CHECK_ARG(batch >= 1 && seq >= 1 && heads >= 1, ZQ_ERR_SHAPE, "bad attention shape");
-  ZQ_CHECK_ARG(head_dim == kAttD, ZQ_ERR_UNSUPPORTED, "fused attention supports head_dim == 64");
+  ZQ_CHECK_ARG(ld_qkv % 4 == 0 && ld_ctx % 4 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
+               ZQ_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
+  if (head_dim != kAttD) {  // CUDA-core flash attention for the other head sizes
+    ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
+                 "attention supports head_dim 64 (tensor cores) or a multiple of 32 up to 256");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e2;
+    switch (head_dim) {
+      case 32: e2 = launch_att_general<32>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 96: e2 = launch_att_general<96>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 128: e2 = launch_att_general<128>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 160: e2 = launch_att_general<160>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 192: e2 = launch_att_general<192>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 224: e2 = launch_att_general<224>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      default: e2 = launch_att_general<256>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+    }
+    if (e2 != cudaSuccess) {
+      set_error("attention launch: %s", cudaGetErrorString(e2));
+      return ZQ_ERR_CUDA;
+    }
+    return ZQ_OK;
+  }
   ZQ_CHECK_ARG(ld_qkv % 4 == 0 && ld_ctx % 4 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                ZQ_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");

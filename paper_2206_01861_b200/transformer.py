@@ -270,35 +270,23 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int,
     [batch*t, d] rows (each sequence attends only to itself).
 
     q, k, v are column views of one [T, 3d] qkv buffer (as produced by the fused
-    QKV GEMM): then the fused tcgen05 kernel (zq_attention_f32, 3xTF32 split,
-    ~fp32 accuracy; online softmax over 128-key blocks for t > 128) runs for head_dim 64; other head sizes use torch's
-    float32 scaled-dot-product attention."""
+    QKV GEMM; separate tensors are packed first).  head_dim 64: the tcgen05
+    kernels (fp16 two-term split for t <= 128, 3xTF32 online softmax beyond);
+    other head sizes (multiples of 32 up to 256, e.g. GPT-J 256, NeoX 96): the
+    CUDA-core fp32 flash-attention kernel.  Anything else raises."""
     bt, d = q.shape
     t = bt // batch
     dh = d // num_heads
     scale = float(np.float32(1.0 / math.sqrt(dh)))
-    fused = (dh == 64 and q.stride(1) == 1 and k.data_ptr() == q.data_ptr() + 4 * d
-             and v.data_ptr() == q.data_ptr() + 8 * d and q.stride(0) == k.stride(0) == v.stride(0))
-    if fused:
-        ctx = out if out is not None else torch.empty((bt, d), dtype=torch.float32, device=q.device)
-        lib = N.load()
-        rc = lib.zq_attention_f32(q.data_ptr(), q.stride(0), batch, t, num_heads, dh, int(causal),
-                                  scale, ctx.data_ptr(), ctx.stride(0), N.stream_ptr())
-        if rc == N.ZQ_OK:
-            return ctx
-        if rc != N.ZQ_ERR_UNSUPPORTED:
-            N.check(rc)
-
-    def heads(z):
-        return z.reshape(batch, t, num_heads, dh).transpose(1, 2)
-
-    ctx = torch.nn.functional.scaled_dot_product_attention(
-        heads(q), heads(k), heads(v), is_causal=causal, scale=scale)
-    ctx = ctx.transpose(1, 2).reshape(bt, d)
-    if out is not None:
-        out.copy_(ctx)
-        return out
-    return ctx.contiguous()
+    packed = (q.stride(1) == 1 and k.data_ptr() == q.data_ptr() + 4 * d
+              and v.data_ptr() == q.data_ptr() + 8 * d and q.stride(0) == k.stride(0) == v.stride(0))
+    if not packed:
+        qkv = torch.cat([q, k, v], dim=1).contiguous()
+        q = qkv[:, :d]
+    ctx = out if out is not None else torch.empty((bt, d), dtype=torch.float32, device=q.device)
+    N.call("zq_attention_f32", q.data_ptr(), q.stride(0), batch, t, num_heads, dh, int(causal), scale,
+           ctx.data_ptr(), ctx.stride(0), N.stream_ptr())
+    return ctx
 
 
 def _linear_site(x, w: QuantizedMatrix, bias, am):

@@ -37,3 +37,31 @@ def test_fused_attention_close_to_f64(seq, causal):
     # blocks (seq > 128) adds one rescale rounding per block
     tol = 1e-5 if seq <= 128 else 3e-5
     assert rel < tol and err < 1e-4, (rel, err)
+
+
+@pytest.mark.parametrize("dh,heads,seq", [(256, 4, 128), (96, 8, 128), (96, 4, 77), (32, 6, 40), (128, 2, 300),
+                                          (256, 2, 1)])
+@pytest.mark.parametrize("causal", [True, False])
+def test_general_head_dim_attention_close_to_f64(dh, heads, seq, causal):
+    """Head sizes other than 64 (GPT-J 256, NeoX 96): CUDA-core fp32 flash kernel."""
+    from paper_2206_01861_b200 import transformer as T
+
+    batch = 3
+    d = heads * dh
+    torch.manual_seed(dh + seq + causal)
+    qkv = torch.randn(batch * seq, 3 * d, device="cuda") * 1.5
+    out = T.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], heads, causal, batch)
+    ref = ref_attention(qkv, batch, seq, heads, dh, causal)
+    rel = ((out.double() - ref).norm() / ref.norm()).item()
+    err = (out.double() - ref).abs().max().item()
+    assert rel < 2e-6 and err < 2e-5, (rel, err)
+
+
+def test_attention_separate_qkv_tensors_are_packed():
+    from paper_2206_01861_b200 import transformer as T
+
+    torch.manual_seed(1)
+    q, k, v = (torch.randn(2 * 32, 4 * 64, device="cuda") for _ in range(3))
+    out = T.attention(q, k, v, 4, False, 2)
+    ref = ref_attention(torch.cat([q, k, v], 1), 2, 32, 4, 64, False)
+    assert ((out.double() - ref).norm() / ref.norm()).item() < 1e-5
