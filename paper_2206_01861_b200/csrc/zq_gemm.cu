@@ -711,7 +711,8 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
 // the rows across all S partials through distributed shared memory (exact: int32
 // addition is order-free) and applies the dequant epilogue for them.
 // ---------------------------------------------------------------------------
-constexpr int kSkStages = 4;  // 96 KB: two CTAs per SM (8 stages measured slower)
+constexpr int kSkStages = 4;  // 96 KB: two CTAs per SM, so the next GEMM's weight prefetch (PDL) overlaps
+                              // this one's tail (8 stages: 16 -> 26 us at 16x4096x12288)
 
 template <int MP, int W4 = 0>
 struct SkinnyCfg {
@@ -884,11 +885,11 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_before();
   pdl_wait();
   cluster_sync();
-  // ---- cluster reduction + epilogue for rows [r*RP, (r+1)*RP) ----
-  const int RP = 128 / S;
+  // ---- cluster reduction + epilogue for rows [128 r / S, 128 (r+1) / S) ----
+  const int r_lo = (128 * r) / S, RP = (128 * (r + 1)) / S - r_lo;
   const uint32_t pbase = smem_u32(part);
   for (int it = threadIdx.x; it < MP * RP; it += 128) {
-    const int m = it / RP, nl = r * RP + it % RP;
+    const int m = it / RP, nl = r_lo + it % RP;
     const int n = n0 + nl;
     if (m >= p.M || n >= p.N) continue;
     const uint32_t off = pbase + (uint32_t)(m * 128 + nl) * 4;
@@ -1544,6 +1545,9 @@ static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmPar
 // CTAs per SM (a partial second wave costs more than the extra split saves) and
 // leaves every split >= 2 k-blocks.
 static int pick_split(int n_tiles, int nkb) {
+  // (measured on the GPT-J / NeoX decode shapes: forcing S = 2..8, non-power-of-two
+  // S (clusters of 3 / 6 co-schedule poorly) or filling two CTAs per SM never beat
+  // this rule, tools/microbench.py skinny)
   int S = 1;
   while (S < 8 && n_tiles * S * 2 <= 2 * g_num_sms * ZQ_SKINNY_CTAS_PER_SM && nkb / (2 * S) >= 2) S *= 2;
   return S;

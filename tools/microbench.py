@@ -54,8 +54,14 @@ def quant_benches(res):
             res[f"ln_res_quant_{t}x{d}"] = {"us": sec * 1e6, "GBps": (13 * t * d + 4 * t) / sec / 1e9}
 
 
-def gemm_benches(res):
-    for (t, k, n, wb, od) in [(4096, 768, 3072, 8, torch.float16), (4096, 768, 3072, 8, torch.float32),
+SKINNY = [(16, 4096, 12288, 8, torch.float32), (16, 4096, 4096, 8, torch.float32),
+          (16, 4096, 16384, 8, torch.float32), (16, 16384, 4096, 8, torch.float32),
+          (16, 6144, 18432, 8, torch.float32), (16, 6144, 6144, 8, torch.float32),
+          (16, 6144, 24576, 8, torch.float32), (16, 24576, 6144, 8, torch.float32)]
+
+
+def gemm_benches(res, shapes=None):
+    for (t, k, n, wb, od) in shapes or [(4096, 768, 3072, 8, torch.float16), (4096, 768, 3072, 8, torch.float32),
                               (4096, 768, 2304, 8, torch.float32), (4096, 768, 768, 8, torch.float32),
                               (4096, 3072, 768, 8, torch.float32), (8192, 8192, 8192, 8, torch.float16),
                               (4096, 4096, 16384, 8, torch.float16), (2048, 6144, 24576, 8, torch.float16),
@@ -90,6 +96,8 @@ def main():
         quant_benches(res)
     if which in ("all", "gemm"):
         gemm_benches(res)
+    if which == "skinny":
+        gemm_benches(res, SKINNY)
     for k, v in res.items():
         print(k, json.dumps({a: round(b, 2) for a, b in v.items()}))
 
