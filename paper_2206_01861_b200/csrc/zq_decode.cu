@@ -35,13 +35,14 @@ __global__ void kv_append_kernel(const float* __restrict__ qkv, int64_t ld_qkv, 
 }
 
 // Flash-decoding: a cluster of C CTAs per (sequence, head); CTA c takes the
-// keys [c*chunk, (c+1)*chunk) below lens[b] and produces a partial
-// (max m_c, sum l_c, unnormalised o_c = sum_j e^(s_j - m_c) v_j); after a cluster
-// barrier each CTA combines dims [c*dh/C, (c+1)*dh/C) of all C partials through
-// distributed shared memory:  o = sum_c o_c e^(m_c - M) / sum_c l_c e^(m_c - M).
-// 256 threads; scores: 8 lanes per key (4 keys per warp step, float4 chunks,
-// xor-reduce); P.V: G = 256/(dh/4) key groups of dh/4 threads (float4 of dims).
-constexpr int kDecThreads = 256;
+// keys [c*chunk, (c+1)*chunk) below lens[b].  Inside a CTA every warp runs its
+// own online softmax over keys c*chunk + warp, + 4, ... (four keys per step: the
+// K and V rows of all four are loaded before any is used, so each warp keeps
+// 8-16 KB of the cache in flight and K and V stream together), q stays in
+// registers, scores are dot products reduced across the warp.  The four warp
+// partials (m, l, o) are merged in shared memory, then each CTA combines dims
+// [c*dh/C, (c+1)*dh/C) of the C partials through distributed shared memory:
+//   o = sum_c o_c 2^(m_c - M) / sum_c l_c 2^(m_c - M)   (scores in log2 units).
 
 __device__ __forceinline__ uint32_t dsm_map(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -61,128 +62,138 @@ __device__ __forceinline__ uint32_t cta_rank_in_cluster() {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ float ex2f(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 
-__global__ void __launch_bounds__(kDecThreads) decode_attention_kernel(
+// THREADS per CTA; LPK lanes per key, NF float4 chunks of the head per lane
+// (LPK < 32: a warp runs 32 / LPK independent "virtual warps", so no lane idles:
+// head_dim 64 -> 16 x 1, 96 -> 8 x 3, 128 -> 32 x 1, 256 -> 32 x 2); U keys per
+// virtual-warp step have their K / V rows in flight together
+template <int THREADS, int LPK, int NF, int U>
+__global__ void __launch_bounds__(THREADS) decode_attention_kernel(
     const float* __restrict__ q, int64_t ld_q, const float* __restrict__ kc,
     const float* __restrict__ vc, int64_t max_ctx, int heads, int dh,
     const int32_t* __restrict__ lens, float scale, float* __restrict__ ctx, int64_t ld_ctx,
     int C, int chunk) {
-  extern __shared__ float dsm[];
-  __shared__ float red[32];
-  __shared__ float stat[2];  // m_c, l_c
+  constexpr int NVW = (THREADS / 32) * (32 / LPK);  // virtual warps
+  __shared__ __align__(16) float po[NVW][256];      // partial outputs; row 0 = o_c
+  __shared__ float wst[NVW][2];
+  __shared__ float stat[2];  // m_c, l_c (log2 units)
   pdl_trigger();
   pdl_wait();
   const int c = (int)cta_rank_in_cluster();
   const int bh = blockIdx.x / C;
   const int b = bh / heads, h = bh % heads;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int dl = heads * dh;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int vw = tid / LPK, sl = tid % LPK;
+  const int dl = heads * dh, d4 = dh >> 2;
   const int len = lens[b];
   const int j0 = c * chunk, j1 = min(len, j0 + chunk);
-  const int G = kDecThreads / (dh >> 2);
-  float* sq = dsm;                 // [dh]
-  float* sc = dsm + 256;           // [chunk]
-  float* po = sc + chunk;          // [G][dh] partial outputs; row 0 = o_c after the reduce
-  for (int i = tid; i < dh; i += kDecThreads) sq[i] = q[(int64_t)b * ld_q + h * dh + i];
-  __syncthreads();
-
-  const int d4 = dh >> 2;
   const float* kb = kc + (int64_t)b * max_ctx * dl + h * dh;
   const float* vb = vc + (int64_t)b * max_ctx * dl + h * dh;
-  {
-    const int sub = lane >> 3, l8 = lane & 7;
-#pragma unroll 2
-    for (int jj = j0 + warp * 4; jj < j1; jj += 4 * (kDecThreads / 32)) {
-      const int j = jj + sub;
-      float acc = 0.0f;
-      if (j < j1) {
-        // issue every load of the key row first (dh <= 256: <= 8 float4 per lane)
-        const float4* kr = reinterpret_cast<const float4*>(kb + (int64_t)j * dl);
-        float4 kv[8];
+  const float sl2 = __fmul_rn(scale, 1.4426950408889634f);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* qr = reinterpret_cast<const float4*>(q + (int64_t)b * ld_q + h * dh);
+  float4 qv[NF], o[NF];
+  bool fo[NF];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          kv[i] = (l8 + 8 * i < d4) ? __ldg(kr + l8 + 8 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < NF; ++i) {
+    fo[i] = sl + LPK * i < d4;
+    qv[i] = fo[i] ? __ldg(qr + sl + LPK * i) : z4;
+    o[i] = z4;
+  }
+  float m = -INFINITY, l = 0.0f;
+  // every virtual warp of a hardware warp runs the same trip count (shuffles)
+  const int wbase = j0 + (vw - (lane / LPK));
+  for (int jw = wbase; jw < j1; jw += U * NVW) {
+    const int jj = jw + lane / LPK;
+    float4 kk[U][NF], vv[U][NF];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (l8 + 8 * i < d4) {
-            const float4 qv = *reinterpret_cast<const float4*>(sq + 4 * (l8 + 8 * i));
-            acc = __fmaf_rn(qv.x, kv[i].x, acc);
-            acc = __fmaf_rn(qv.y, kv[i].y, acc);
-            acc = __fmaf_rn(qv.z, kv[i].z, acc);
-            acc = __fmaf_rn(qv.w, kv[i].w, acc);
-          }
-        }
+    for (int u = 0; u < U; ++u) {
+      const int j = jj + u * NVW;
+      const bool ok = j < j1;
+      const float4* kr = reinterpret_cast<const float4*>(kb + (int64_t)j * dl);
+      const float4* vr = reinterpret_cast<const float4*>(vb + (int64_t)j * dl);
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        kk[u][i] = ok && fo[i] ? __ldg(kr + sl + LPK * i) : z4;
+        vv[u][i] = ok && fo[i] ? __ldg(vr + sl + LPK * i) : z4;
       }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      if (l8 == 0 && j < j1) sc[j - j0] = __fmul_rn(acc, scale);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float d = 0.0f;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        d = __fmaf_rn(qv[i].x, kk[u][i].x, d);
+        d = __fmaf_rn(qv[i].y, kk[u][i].y, d);
+        d = __fmaf_rn(qv[i].z, kk[u][i].z, d);
+        d = __fmaf_rn(qv[i].w, kk[u][i].w, d);
+      }
+#pragma unroll
+      for (int off = LPK / 2; off > 0; off >>= 1) d = __fadd_rn(d, __shfl_xor_sync(0xffffffffu, d, off));
+      if (jj + u * NVW < j1) {
+        const float sv = __fmul_rn(d, sl2);
+        const float mn = fmaxf(m, sv);
+        const float corr = ex2f(__fsub_rn(m, mn));  // m = -inf -> 0
+        const float pj = ex2f(__fsub_rn(sv, mn));
+        l = __fmaf_rn(l, corr, pj);
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+          o[i].x = __fmaf_rn(pj, vv[u][i].x, __fmul_rn(o[i].x, corr));
+          o[i].y = __fmaf_rn(pj, vv[u][i].y, __fmul_rn(o[i].y, corr));
+          o[i].z = __fmaf_rn(pj, vv[u][i].z, __fmul_rn(o[i].z, corr));
+          o[i].w = __fmaf_rn(pj, vv[u][i].w, __fmul_rn(o[i].w, corr));
+        }
+        m = mn;
+      }
     }
   }
-  __syncthreads();
-  float mx = -INFINITY;
-  for (int j = tid; j < j1 - j0; j += kDecThreads) mx = fmaxf(mx, sc[j]);
-  mx = warp_max(mx);
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  mx = red[0];
 #pragma unroll
-  for (int w = 1; w < kDecThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  for (int i = 0; i < NF; ++i)
+    if (fo[i]) *reinterpret_cast<float4*>(&po[vw][4 * (sl + LPK * i)]) = o[i];
+  if (sl == 0) wst[vw][0] = m, wst[vw][1] = l;
   __syncthreads();
-  float sum = 0.0f;
-  for (int j = tid; j < j1 - j0; j += kDecThreads) {
-    const float e = expf(sc[j] - mx);
-    sc[j] = e;
-    sum += e;
-  }
+  // merge the virtual-warp partials: M = max m_w, L = sum l_w 2^(m_w - M), o_c = sum o_w 2^(m_w - M)
+  float M = -INFINITY;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  if (lane == 0) red[warp] = sum;
-  __syncthreads();
-  if (tid == 0) {
-    float t = 0.0f;
-    for (int w = 0; w < kDecThreads / 32; ++w) t += red[w];
-    stat[0] = mx;  // -inf for an empty chunk
-    stat[1] = t;
-  }
-  const int g = tid / d4, cc = tid % d4;
-  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (g < G) {
-#pragma unroll 8
-    for (int j = j0 + g; j < j1; j += G) {
-      const float pj = sc[j - j0];
-      const float4 v = __ldg(reinterpret_cast<const float4*>(vb + (int64_t)j * dl) + cc);
-      o.x = __fmaf_rn(pj, v.x, o.x);
-      o.y = __fmaf_rn(pj, v.y, o.y);
-      o.z = __fmaf_rn(pj, v.z, o.z);
-      o.w = __fmaf_rn(pj, v.w, o.w);
-    }
-    *reinterpret_cast<float4*>(po + g * dh + 4 * cc) = o;
+  for (int w = 0; w < NVW; ++w) M = fmaxf(M, wst[w][0]);
+  float fw[NVW];
+  float L = 0.0f;
+#pragma unroll
+  for (int w = 0; w < NVW; ++w) {
+    fw[w] = wst[w][0] == -INFINITY ? 0.0f : ex2f(__fsub_rn(wst[w][0], M));
+    L = __fmaf_rn(wst[w][1], fw[w], L);
   }
   __syncthreads();
-  for (int i = tid; i < dh; i += kDecThreads) {
+  for (int i = tid; i < dh; i += THREADS) {
     float t = 0.0f;
-    for (int gg = 0; gg < G; ++gg) t += po[gg * dh + i];
-    po[i] = t;  // row 0 of po = o_c
+#pragma unroll
+    for (int w = 0; w < NVW; ++w) t = __fmaf_rn(po[w][i], fw[w], t);
+    po[0][i] = t;
   }
+  if (tid == 0) stat[0] = M, stat[1] = L;  // M = -inf for an empty chunk
   cluster_barrier();
   // combine dims [c*dh/C, (c+1)*dh/C) across the cluster
   const int da = (c * dh) / C, db = ((c + 1) * dh) / C;
-  const uint32_t stat_a = smem_u32(stat), po_a = smem_u32(po);
-  float M = -INFINITY;
-  for (int r = 0; r < C; ++r) M = fmaxf(M, dsm_ld_f32(dsm_map(stat_a, r)));
-  float L = 0.0f;
+  const uint32_t stat_a = smem_u32(stat), po_a = smem_u32(&po[0][0]);
+  float MM = -INFINITY;
+  for (int r = 0; r < C; ++r) MM = fmaxf(MM, dsm_ld_f32(dsm_map(stat_a, r)));
+  float LL = 0.0f;
   for (int r = 0; r < C; ++r) {
     const float mr = dsm_ld_f32(dsm_map(stat_a, r));
-    if (mr != -INFINITY) L += dsm_ld_f32(dsm_map(stat_a + 4, r)) * expf(mr - M);
+    if (mr != -INFINITY) LL += dsm_ld_f32(dsm_map(stat_a + 4, r)) * ex2f(mr - MM);
   }
-  for (int i = da + tid; i < db; i += kDecThreads) {
+  for (int i = da + tid; i < db; i += THREADS) {
     float t = 0.0f;
     for (int r = 0; r < C; ++r) {
       const float mr = dsm_ld_f32(dsm_map(stat_a, r));
-      if (mr != -INFINITY) t += dsm_ld_f32(dsm_map(po_a + 4 * i, r)) * expf(mr - M);
+      if (mr != -INFINITY) t += dsm_ld_f32(dsm_map(po_a + 4 * i, r)) * ex2f(mr - MM);
     }
-    ctx[(int64_t)b * ld_ctx + h * dh + i] = t / L;
+    ctx[(int64_t)b * ld_ctx + h * dh + i] = t / LL;
   }
   cluster_barrier();  // keep this CTA's partial alive until every peer has read it
 }
@@ -219,23 +230,38 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
   ZQ_CHECK_ARG(batch >= 1 && heads >= 1 && max_ctx >= 1, ZQ_ERR_SHAPE, "bad decode attention shape");
   ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
                "decode attention supports head_dim % 32 == 0 and <= 256");
-  // context chunks per (sequence, head): split until ~4 CTAs per SM are in flight,
-  // at most 8 (portable cluster), keeping >= 32 keys per chunk
+  // context chunks per (sequence, head): split until ~1000 CTAs of 4 warps are in
+  // flight (7 per SM), at most 8 (portable cluster), keeping >= 16 keys per chunk
   int C = 1;
-  while (C < 8 && (int64_t)batch * heads * C < 4 * 148 && max_ctx / (2 * C) >= 32) C *= 2;
-  const int chunk = (int)(((max_ctx + C - 1) / C + 3) / 4 * 4);  // keeps the partial-output rows 16-byte aligned
-  const int G = kDecThreads / (head_dim / 4);
-  const size_t smem = sizeof(float) * (256 + (size_t)chunk + (size_t)G * head_dim);
-  ZQ_CHECK_ARG(smem <= 200 * 1024, ZQ_ERR_UNSUPPORTED, "context too long for decode attention");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
+  while (C < 8 && (int64_t)batch * heads * C * 2 <= 7 * 148 && max_ctx / (2 * C) >= 16) C *= 2;
+  {
+    static int force = -1;
+    if (force < 0) {
+      const char* ev = getenv("ZQ_DEC_C");
+      force = ev ? atoi(ev) : 0;
+    }
+    if (force >= 1 && force <= 8) C = force;
   }
-  cudaError_t e = launch_kernel(decode_attention_kernel, dim3(batch * heads * C), dim3(kDecThreads), smem,
-                                reinterpret_cast<cudaStream_t>(stream), C, q, ld_q, kcache, vcache,
-                                max_ctx, heads, head_dim, lens, scale, ctx, ld_ctx, C, chunk);
+  const int chunk = (int)((max_ctx + C - 1) / C);
+  static int wide_env = -1;
+  if (wide_env < 0) {
+    const char* ev = getenv("ZQ_DEC_WIDE");
+    wide_env = ev ? atoi(ev) : 0;
+  }
+  const bool wide = wide_env == 1;
+  cudaError_t e;
+#define ZQ_DEC(TT, LL, NN, UU)                                                                           \
+  e = launch_kernel(decode_attention_kernel<TT, LL, NN, UU>, dim3(batch * heads * C), dim3(TT), 0,      \
+                    reinterpret_cast<cudaStream_t>(stream), C, q, ld_q, kcache, vcache, max_ctx, heads,  \
+                    head_dim, lens, scale, ctx, ld_ctx, C, chunk)
+  (void)wide;
+  const int d4 = head_dim / 4;
+  if (d4 <= 8) ZQ_DEC(128, 8, 1, 2);
+  else if (d4 <= 16) ZQ_DEC(128, 16, 1, 2);
+  else if (d4 <= 24) ZQ_DEC(128, 8, 3, 1);
+  else if (d4 <= 32) ZQ_DEC(128, 32, 1, 2);
+  else ZQ_DEC(128, 32, 2, 2);
+#undef ZQ_DEC
   if (e != cudaSuccess) {
     set_error("decode attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;

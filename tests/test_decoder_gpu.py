@@ -81,7 +81,7 @@ def test_prefill_and_cached_decode_match_recompute(mbits, fbits):
 def test_decode_attention_vs_torch():
     from paper_2206_01861_b200 import _native as N
 
-    for dh, heads in ((64, 4), (96, 3), (256, 2)):
+    for dh, heads in ((64, 4), (96, 3), (256, 2), (32, 5), (128, 2)):
         batch, max_ctx = 3, 1041  # odd context: chunked over a cluster
         dl = dh * heads
         torch.manual_seed(dh)
