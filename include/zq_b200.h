@@ -179,6 +179,17 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
                             const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
                             void* stream);
 
+/* Tied LM head + greedy argmax of a decode step (logits = x @ emb^T, argmax per
+ * row; float, tolerance parity): x [ntok <= 16, dim] f32 (row stride ld_x),
+ * emb [vocab, dim] f32 row-major, emb_scale = a power of two with
+ * max|emb| * emb_scale in [2^14, 2^15) (chosen once by the caller).  tcgen05
+ * kind::f16 on a two-term f16 split of both operands (~fp32 accuracy); ties
+ * resolve to the lowest index (numpy argmax).  Workspaces: xh_ws / xl_ws
+ * 16*dim f16 each, xinv_ws 16 f32, keys_ws 16 u64.  ids: int64 [ntok]. */
+int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, int64_t vocab, int64_t dim,
+                      float emb_scale, void* xh_ws, void* xl_ws, float* xinv_ws, unsigned long long* keys_ws,
+                      int64_t* ids, void* stream);
+
 /* Diagnostics / tests: the fp32 GeLU estimate the quantizer brackets with, and
  * its per-element relative error bound (x clamped to >= -5.5). */
 int zq_gelu_estimate(const float* x, int64_t n, float* est, float* bound, void* stream);

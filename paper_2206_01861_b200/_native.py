@@ -48,6 +48,7 @@ _SIGS = {
     "zq_attention_f32": [_p, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _p, _i64, _p],
     "zq_kv_append": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _p],
     "zq_decode_attention_f32": [_p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p, _f32, _p, _i64, _p],
+    "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
 }
 
 _lock = threading.Lock()

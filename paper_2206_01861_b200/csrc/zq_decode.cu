@@ -9,6 +9,8 @@
 // with causal attention and token-wise activation scales the cached k / v rows
 // are exactly the rows that recomputation would produce, so caching changes no
 // value — only float attention (tolerance parity) runs here.
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <string.h>
 
 #include "zq_common.cuh"
@@ -198,9 +200,260 @@ __global__ void __launch_bounds__(THREADS) decode_attention_kernel(
   cluster_barrier();  // keep this CTA's partial alive until every peer has read it
 }
 
+// ---------------------------------------------------------------------------
+// Tied LM head + greedy argmax for a decode step (evaluate.py's logits =
+// LN(x_last) @ E^T, argmax per sequence; float, tolerance parity):
+//   prep   : per token, x -> power-of-two scale (max in [2^14, 2^15)) and f16
+//            hi / lo rows (two-term split, 22 significant bits); keys zeroed
+//   main   : persistent CTAs walk 128-row vocabulary tiles; a TMA warp streams
+//            the f32 embedding tile by 64-column k-blocks, 4 converter warps
+//            scale (one global power of two) and split it into f16 hi / lo
+//            SWIZZLE_128B tiles, one warp issues tcgen05 kind::f16 MMAs
+//            (E_hi x_hi + E_hi x_lo + E_lo x_hi; M = 128 vocab rows, N = 16
+//            tokens) into a double-buffered TMEM accumulator; the converter
+//            warps then read the 128 x 16 logits and fold them into a per-token
+//            64-bit atomic max of (ordered logit bits, ~index): largest logit,
+//            lowest index on ties — numpy's argmax rule
+//   final  : keys -> int64 token ids
+// The embedding streams from HBM once per step at up to the copy rate; the split
+// costs ~4 FP32 ops per weight element on otherwise idle CUDA cores.
+// ---------------------------------------------------------------------------
+constexpr int kLmRows = 128, kLmK = 64, kLmS1 = 4, kLmS2 = 2, kLmTok = 16;
+constexpr int kLmF32Stage = kLmRows * kLmK * 4;      // 32 KB: two [128 x 32] f32 boxes
+constexpr int kLmOpE = kLmRows * kLmK * 2;           // 16 KB f16 tile
+constexpr int kLmOpX = kLmTok * kLmK * 2;            // 2 KB
+constexpr int kLmOpStage = 2 * kLmOpE + 2 * kLmOpX;  // 36 KB
+constexpr int kLmSmem = kLmS1 * kLmF32Stage + kLmS2 * kLmOpStage + 256;
+
+__device__ __forceinline__ float lm_pow2_scale(uint32_t max_bits) {  // max * f in [2^14, 2^15)
+  const int E = (int)((max_bits >> 23) & 0xFF);
+  int F = 268 - E;
+  F = F < 1 ? 1 : (F > 254 ? 254 : F);
+  return __uint_as_float((uint32_t)F << 23);
+}
+__device__ __forceinline__ void lm_split(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(__fsub_rn(a, hf.x), __fsub_rn(b, hf.y));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+__global__ void __launch_bounds__(256) lm_prep_kernel(const float* __restrict__ x, int64_t ld_x, int ntok, int dim,
+                                                      __half* __restrict__ xh, __half* __restrict__ xl,
+                                                      float* __restrict__ xinv,
+                                                      unsigned long long* __restrict__ keys) {
+  __shared__ uint32_t red[32];
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  const bool act = t < ntok;
+  const float* xr = x + (int64_t)t * ld_x;
+  uint32_t mb = 0;
+  if (act)
+    for (int i = threadIdx.x; i < dim; i += 256) mb = max(mb, __float_as_uint(xr[i]) & 0x7fffffffu);
+  const float f = lm_pow2_scale(__float_as_uint(block_max_nonneg(__uint_as_float(mb), red)));
+  for (int i = 2 * threadIdx.x; i < dim; i += 512) {
+    uint32_t hi = 0, lo = 0;
+    if (act) lm_split(__fmul_rn(xr[i], f), __fmul_rn(xr[i + 1], f), hi, lo);
+    *reinterpret_cast<uint32_t*>(xh + (int64_t)t * dim + i) = hi;
+    *reinterpret_cast<uint32_t*>(xl + (int64_t)t * dim + i) = lo;
+  }
+  if (threadIdx.x == 0) {
+    xinv[t] = __uint_as_float((uint32_t)(254 - (int)(__float_as_uint(f) >> 23)) << 23);
+    keys[t] = 0ull;
+  }
+}
+
+__device__ __forceinline__ void mma_f16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(192, 1)
+    lm_head_kernel(const __grid_constant__ CUtensorMap tmE, const __half* __restrict__ xh,
+                   const __half* __restrict__ xl, const float* __restrict__ xinv, int ntok, int64_t vocab,
+                   int dim, float fe, float inv_fe, unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sF = smem;                                 // [S1] f32 stages
+  uint8_t* sO = smem + kLmS1 * kLmF32Stage;           // [S2] {Eh, El, Xh, Xl}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + kLmS2 * kLmOpStage);
+  uint64_t* f_full = bars;                  // [S1]
+  uint64_t* f_empty = bars + kLmS1;         // [S1]
+  uint64_t* o_full = bars + 2 * kLmS1;      // [S2]
+  uint64_t* o_empty = o_full + kLmS2;       // [S2]
+  uint64_t* t_full = o_empty + kLmS2;       // [2]
+  uint64_t* t_empty = t_full + 2;           // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (int)((vocab + kLmRows - 1) / kLmRows);
+  const int nkb = dim / kLmK;
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    prefetch_tmap(&tmE);
+    for (int i = 0; i < kLmS1; ++i) mbar_init(&f_full[i], 1), mbar_init(&f_empty[i], 4);
+    for (int i = 0; i < kLmS2; ++i) mbar_init(&o_full[i], 4), mbar_init(&o_empty[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&t_full[i], 1), mbar_init(&t_empty[i], 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 32);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  if (warp == 0) {
+    // ---- TMA producer: f32 embedding k-blocks (the weights do not depend on the
+    // previous kernel: the first stages go out before the grid dependency) ----
+    int st = 0, ph = 0;
+    bool waited = false;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&f_empty[st], ph ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&f_full[st], kLmF32Stage);
+          tma_load_2d(sF + st * kLmF32Stage, &tmE, &f_full[st], kb * kLmK, tile * kLmRows);
+          tma_load_2d(sF + st * kLmF32Stage + kLmF32Stage / 2, &tmE, &f_full[st], kb * kLmK + 32, tile * kLmRows);
+        }
+        __syncwarp();
+        if (++st == kLmS1) st = 0, ph ^= 1;
+        (void)waited;
+      }
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    pdl_wait();
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(kLmTok >> 3) << 17) | ((uint32_t)(kLmRows >> 4) << 24);
+    int st = 0, ph = 0, acc = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&t_empty[acc], aph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&o_full[st], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          uint8_t* o = sO + st * kLmOpStage;
+          const uint64_t dEh = make_sw128_desc(smem_u32(o)), dEl = make_sw128_desc(smem_u32(o + kLmOpE));
+          const uint64_t dXh = make_sw128_desc(smem_u32(o + 2 * kLmOpE));
+          const uint64_t dXl = make_sw128_desc(smem_u32(o + 2 * kLmOpE + kLmOpX));
+#pragma unroll
+          for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+            for (int ks = 0; ks < kLmK / 16; ++ks)
+              mma_f16_ss(tmem + acc * 16, (t3 == 2 ? dEl : dEh) + 2 * ks, (t3 == 1 ? dXl : dXh) + 2 * ks, idesc,
+                         (kb | ks | t3) != 0);
+          mma_commit(&o_empty[st]);
+        }
+        __syncwarp();
+        if (++st == kLmS2) st = 0, ph ^= 1;
+      }
+      if (lane == 0) mma_commit(&t_full[acc]);
+      __syncwarp();
+      if (++acc == 2) acc = 0, aph ^= 1;
+    }
+  } else {
+    // ---- converters (row r = thread - 64) and epilogue ----
+    pdl_wait();
+    const int r = threadIdx.x - 64, quarter = warp & 3;
+    int fs = 0, fph = 0, os = 0, oph = 0, acc = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&f_full[fs], fph);
+        mbar_wait(&o_empty[os], oph ^ 1);
+        const uint8_t* fsrc = sF + fs * kLmF32Stage;
+        uint8_t* o = sO + os * kLmOpStage;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {  // 16 float4 chunks: box c / 8, chunk c % 8
+          const float4 v = *reinterpret_cast<const float4*>(fsrc + (c >> 3) * (kLmF32Stage / 2) + r * 128 +
+                                                             (((c & 7) ^ (r & 7)) << 4));
+          lm_split(__fmul_rn(v.x, fe), __fmul_rn(v.y, fe), hi[2 * c], lo[2 * c]);
+          lm_split(__fmul_rn(v.z, fe), __fmul_rn(v.w, fe), hi[2 * c + 1], lo[2 * c + 1]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 8 x 16 B per 128-byte f16 row
+          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(o + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+          *reinterpret_cast<uint4*>(o + kLmOpE + off) =
+              make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+        }
+        {  // the tokens' f16 k-block: 16 rows x 8 chunks = 128 threads x 16 B each
+          const int xr = r >> 3, c = r & 7;
+          const uint32_t off = xr * 128 + ((c ^ (xr & 7)) << 4);
+          const int64_t src = (int64_t)xr * dim + kb * kLmK + 8 * c;
+          *reinterpret_cast<uint4*>(o + 2 * kLmOpE + off) = *reinterpret_cast<const uint4*>(xh + src);
+          *reinterpret_cast<uint4*>(o + 2 * kLmOpE + kLmOpX + off) = *reinterpret_cast<const uint4*>(xl + src);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&f_empty[fs]);
+          mbar_arrive(&o_full[os]);
+        }
+        if (++fs == kLmS1) fs = 0, fph ^= 1;
+        if (++os == kLmS2) os = 0, oph ^= 1;
+      }
+      // ---- epilogue: 16 logits per vocabulary row -> per-token (max, lowest index) ----
+      mbar_wait(&t_full[acc], aph);
+      tc_fence_after();
+      uint32_t lg[16];
+      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 16, lg);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[acc]);
+      if (++acc == 2) acc = 0, aph ^= 1;
+      const int64_t v = (int64_t)tile * kLmRows + quarter * 32 + lane;
+#pragma unroll
+      for (int t = 0; t < kLmTok; ++t) {
+        if (t >= ntok) break;
+        const float val = __fmul_rn(__fmul_rn(__uint_as_float(lg[t]), inv_fe), xinv[t]);
+        uint32_t u = __float_as_uint(val);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        unsigned long long key = v < vocab ? (((unsigned long long)u << 32) | (0xFFFFFFFFull - (uint64_t)v)) : 0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key, off);
+          key = o2 > key ? o2 : key;
+        }
+        if (lane == 0 && key) atomicMax(keys + t, key);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 32);
+}
+
+__global__ void lm_final_kernel(const unsigned long long* __restrict__ keys, int ntok, int64_t* __restrict__ ids) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = threadIdx.x;
+  if (t < ntok) ids[t] = (int64_t)(0xFFFFFFFFull - (keys[t] & 0xFFFFFFFFull));
+}
+
 }  // namespace zq
 
 using namespace zq;
+
+namespace zq {
+int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
+                  int box_cols, int box_rows, CUtensorMapSwizzle sw);
+}
 
 extern "C" {
 
@@ -218,6 +471,49 @@ int zq_kv_append(const float* qkv, int64_t ld_qkv, int batch, int rows_per_seq, 
                                       rows_per_seq, dmodel_local, pos, kcache, vcache, max_ctx, total4);
   if (e != cudaSuccess) {
     set_error("kv append launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, int64_t vocab, int64_t dim,
+                      float emb_scale, void* xh_ws, void* xl_ws, float* xinv_ws, unsigned long long* keys_ws,
+                      int64_t* ids, void* stream) {
+  ZQ_CHECK_ARG(ntok >= 1 && ntok <= kLmTok, ZQ_ERR_UNSUPPORTED, "lm head: 1..16 tokens per step");
+  ZQ_CHECK_ARG(dim % kLmK == 0 && vocab >= 1, ZQ_ERR_UNSUPPORTED, "lm head: dim must be a multiple of 64");
+  ZQ_CHECK_ARG((reinterpret_cast<uintptr_t>(emb) & 15) == 0 && (reinterpret_cast<uintptr_t>(xh_ws) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xl_ws) & 15) == 0,
+               ZQ_ERR_USAGE, "lm head operands must be 16-byte aligned");
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUtensorMap tm;
+  int rc = make_tmap_f32(&tm, emb, vocab, dim, dim * 4, 32, kLmRows, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != ZQ_OK) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lm_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmem);
+    attr = true;
+  }
+  // emb_scale: the power of two the caller chose once for the embedding
+  const float fe = emb_scale;
+  const float inv_fe = 1.0f / emb_scale;
+  cudaError_t e = launch_kernel(lm_prep_kernel, dim3(kLmTok), dim3(256), 0, st, 1, x, ld_x, ntok, (int)dim,
+                                reinterpret_cast<__half*>(xh_ws), reinterpret_cast<__half*>(xl_ws), xinv_ws, keys_ws);
+  if (e == cudaSuccess) {
+    const int ntiles = (int)((vocab + kLmRows - 1) / kLmRows);
+    e = launch_kernel(lm_head_kernel, dim3(ntiles < nsm ? ntiles : nsm), dim3(192), kLmSmem, st, 1, tm,
+                      reinterpret_cast<const __half*>(xh_ws), reinterpret_cast<const __half*>(xl_ws),
+                      (const float*)xinv_ws, ntok, vocab, (int)dim, fe, inv_fe, keys_ws);
+  }
+  if (e == cudaSuccess) e = launch_kernel(lm_final_kernel, dim3(1), dim3(32), 0, st, 1, (const unsigned long long*)keys_ws, ntok, ids);
+  if (e != cudaSuccess) {
+    set_error("lm head launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
   }
   return ZQ_OK;

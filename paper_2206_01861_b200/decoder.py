@@ -28,6 +28,7 @@ device (no checkpoints are available offline).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,6 +110,15 @@ class DecoderEngine:
         self.lens = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.next_ids = torch.zeros(batch, dtype=torch.int64, device=dev)
+        # LM head (zq_lm_head_argmax): one power-of-two scale for the embedding,
+        # chosen once, and the per-step f16 split / argmax workspaces
+        m = float(self.embedding.abs().max())
+        self.emb_scale = math.ldexp(1.0, 15 - math.frexp(m)[1]) if m > 0 else 1.0
+        self._lm_ok = batch <= 16 and cfg.dim % 64 == 0 and os.environ.get("ZQ_LM_TORCH", "0") != "1"
+        self._lm_ws = dict(xh=torch.zeros(16 * cfg.dim, dtype=torch.float16, device=dev),
+                           xl=torch.zeros(16 * cfg.dim, dtype=torch.float16, device=dev),
+                           xinv=torch.zeros(16, dtype=torch.float32, device=dev),
+                           keys=torch.zeros(16, dtype=torch.int64, device=dev))
         self._bufs: dict[int, dict] = {}
         self._graph = None
         self.scale = float(np.float32(1.0 / math.sqrt(cfg.head_dim)))
@@ -218,8 +228,15 @@ class DecoderEngine:
         B["last"].copy_(last)
         self._ln_quant(B["last"], None, self.final_gamma, self.final_beta, B["out"][: self.batch],
                        B["lq"], B["ls"])
-        torch.matmul(B["out"][: self.batch], self.embedding.t(), out=B["logits"])
-        torch.argmax(B["logits"], dim=1, out=self.next_ids)
+        out = B["out"][: self.batch]
+        if self._lm_ok:  # tcgen05 two-term f16 LM head with a fused argmax
+            W = self._lm_ws
+            N.call("zq_lm_head_argmax", out.data_ptr(), out.stride(0), self.batch, self.embedding.data_ptr(),
+                   self.cfg.vocab, self.cfg.dim, self.emb_scale, W["xh"].data_ptr(), W["xl"].data_ptr(),
+                   W["xinv"].data_ptr(), W["keys"].data_ptr(), self.next_ids.data_ptr(), N.stream_ptr())
+        else:  # batch > 16 (or ZQ_LM_TORCH=1): float32 matmul + argmax
+            torch.matmul(out, self.embedding.t(), out=B["logits"])
+            torch.argmax(B["logits"], dim=1, out=self.next_ids)
 
     def _embed(self, B, ids):
         torch.index_select(self.embedding, 0, ids, out=B["x"])

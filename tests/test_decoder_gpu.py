@@ -4,6 +4,7 @@ oracle recomputing the whole causal context with the reference block
 on both sides, so hidden states are compared with the block tolerance; the
 greedy tokens must agree."""
 
+import math
 import numpy as np
 import pytest
 import torch
@@ -101,3 +102,34 @@ def test_decode_attention_vs_torch():
             p = torch.softmax(qh @ k.transpose(1, 2) * scale, -1)
             ref = (p @ v).reshape(dl)
             assert torch.allclose(ctx[b].double(), ref, rtol=1e-5, atol=1e-5), (dh, b)
+
+
+def test_lm_head_argmax_vs_f64():
+    """zq_lm_head_argmax (tcgen05 two-term f16 split, fused argmax) vs float64
+    logits: same token wherever the top two logits are not a near-tie; exact ties
+    resolve to the lowest index like numpy's argmax."""
+    from paper_2206_01861_b200 import _native as N
+
+    for ntok, vocab, dim in ((16, 3001, 256), (5, 50400, 1024), (1, 129, 64)):
+        torch.manual_seed(vocab)
+        x = torch.randn(ntok, dim, device="cuda")
+        emb = torch.randn(vocab, dim, device="cuda") * 0.02
+        emb[vocab // 2] = emb[vocab - 1] = x[0] * 0.05  # an exact tie for token 0 (largest logit)
+        m = float(emb.abs().max())
+        scale = math.ldexp(1.0, 15 - math.frexp(m)[1])
+        xh = torch.zeros(16 * dim, dtype=torch.float16, device="cuda")
+        xl = torch.zeros_like(xh)
+        xinv = torch.zeros(16, device="cuda")
+        keys = torch.zeros(16, dtype=torch.int64, device="cuda")
+        ids = torch.full((ntok,), -1, dtype=torch.int64, device="cuda")
+        N.call("zq_lm_head_argmax", x.data_ptr(), x.stride(0), ntok, emb.data_ptr(), vocab, dim, scale,
+               xh.data_ptr(), xl.data_ptr(), xinv.data_ptr(), keys.data_ptr(), ids.data_ptr(), N.stream_ptr())
+        logits = x.double() @ emb.double().t()
+        top2 = logits.topk(2, dim=1)
+        ref = logits.argmax(dim=1)
+        got = ids.cpu()
+        assert int(got[0]) == vocab // 2, (int(got[0]), vocab // 2)  # tie -> lowest index
+        for t in range(1, ntok):
+            gap = float(top2.values[t, 0] - top2.values[t, 1])
+            if gap > 1e-5 * abs(float(top2.values[t, 0])):
+                assert int(got[t]) == int(ref[t]), (ntok, vocab, t)
