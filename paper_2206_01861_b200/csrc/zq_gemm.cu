@@ -711,8 +711,10 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
 // the rows across all S partials through distributed shared memory (exact: int32
 // addition is order-free) and applies the dequant epilogue for them.
 // ---------------------------------------------------------------------------
-constexpr int kSkStages = 4;  // 96 KB: two CTAs per SM, so the next GEMM's weight prefetch (PDL) overlaps
-                              // this one's tail (8 stages: 16 -> 26 us at 16x4096x12288)
+// 4 stages = 96 KB: two CTAs per SM, so the next GEMM's weight prefetch (PDL)
+// overlaps this one.  GPT-J decode step, linears in-graph: 2 stages 1.80 ms,
+// 3 stages 1.63, 4 stages 1.59, 6 stages 2.74, 8 stages 2.75 (tools/ablate_decode.py)
+constexpr int kSkStages = 4;
 
 template <int MP, int W4 = 0>
 struct SkinnyCfg {
