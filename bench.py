@@ -567,7 +567,15 @@ def run_gpt(args, rank: int, world: int, dist):
         return orig_att(*a, **kw)
 
     from paper_2206_01861_b200 import decoder as D
-    N.call, D.attention = counting_call, counting_att
+    orig_rc = N.call_rc
+
+    def counting_rc(name, *a):
+        rc = orig_rc(name, *a)
+        if rc == 0:
+            calls["n"] += 1
+        return rc
+
+    N.call, N.call_rc, D.attention = counting_call, counting_rc, counting_att
     try:
         eng.prefill(ids_dev)
         n_prefill = calls["n"]
@@ -575,7 +583,7 @@ def run_gpt(args, rank: int, world: int, dist):
         eng._step_launches()
         n_step = calls["n"]
     finally:
-        N.call, D.attention = orig_call, orig_att
+        N.call, N.call_rc, D.attention = orig_call, orig_rc, orig_att
     torch.cuda.synchronize()
     launches = args.steps * (n_prefill + (new - 1) * n_step)
     if dist is not None:

@@ -171,6 +171,16 @@ int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int h
 int zq_kv_append(const float* qkv, int64_t ld_qkv, int batch, int rows_per_seq, int dmodel_local,
                  const int32_t* pos, float* kcache, float* vcache, int64_t max_ctx, void* stream);
 
+/* Decode QKV projection with the KV-cache append fused into the epilogue: as
+ * zq_linear (f32 output, M <= 64 rows, one row per sequence) and additionally
+ * kcache / vcache[m, pos[m], :] = columns [dl, 2 dl) / [2 dl, 3 dl) of row m
+ * (N == 3 * dmodel_local).  ZQ_ERR_UNSUPPORTED for M > 64 (prefill): call
+ * zq_linear then zq_kv_append. */
+int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                 int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                 float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
+                 int64_t max_ctx, void* stream);
+
 /* One-token-per-sequence attention against the caches (transformer.py:413-440
  * for the last query row): ctx[b, h] = softmax(q.K^T * scale) V over the first
  * lens[b] cached tokens (device int32).  head_dim % 32 == 0, <= 256. */

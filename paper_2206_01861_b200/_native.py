@@ -48,6 +48,8 @@ _SIGS = {
     "zq_attention_f32": [_p, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _p, _i64, _p],
     "zq_kv_append": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _p],
     "zq_decode_attention_f32": [_p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p, _f32, _p, _i64, _p],
+    "zq_linear_kv": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i32, _i64,
+                     _p],
     "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
 }
 
@@ -110,6 +112,15 @@ def check(rc: int) -> None:
 def call(name: str, *args) -> None:
     lib = load()
     check(getattr(lib, name)(*args))
+
+
+def call_rc(name: str, *args) -> int:
+    """Like call() but hands ZQ_ERR_UNSUPPORTED back (for entry points with a
+    caller-side alternative); any other failure raises."""
+    rc = getattr(load(), name)(*args)
+    if rc != ZQ_ERR_UNSUPPORTED:
+        check(rc)
+    return rc
 
 
 def stream_ptr(stream=None) -> int:

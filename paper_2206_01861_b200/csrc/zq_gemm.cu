@@ -49,6 +49,13 @@ struct GemmParams {
   unsigned long long* trace;  // diagnostics: per-CTA %globaltimer stamps (nullable)
   int debug;                  // diagnostics: 1 = skip global stores, 2 = skip dequant math
   int group_m;                // tile rasterisation group (1 = row-major)
+  // decode QKV (skinny path, one row per sequence): columns [dl, 2 dl) / [2 dl, 3 dl)
+  // of row m are also written to kc / vc[m, kv_pos[m], :] (the KV cache append)
+  float* kc;
+  float* vc;
+  const int32_t* kv_pos;
+  int kv_dl;
+  int64_t kv_max_ctx;
 };
 
 __device__ __forceinline__ void bulk_wait_read1() {
@@ -904,9 +911,18 @@ __global__ void __launch_bounds__(128, 1)
       const float st = p.token_scales ? __ldg(p.token_scales + m) : p.static_scale;
       float f = __fmul_rn(__fmul_rn(__int2float_rn(acc), st), __ldg(p.row_scales + n));
       if (p.bias) f = __fadd_rn(f, __ldg(p.bias + n));
-      if (KIND == OUT_F32) reinterpret_cast<float*>(p.out)[o] = f;
-      else if (KIND == OUT_F16) reinterpret_cast<__half*>(p.out)[o] = __float2half_rn(f);
-      else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(f);
+      if (KIND == OUT_F32) {
+        reinterpret_cast<float*>(p.out)[o] = f;
+        if (p.kc != nullptr && n >= p.kv_dl) {  // fused KV-cache append (decode QKV)
+          const int64_t slot = ((int64_t)m * p.kv_max_ctx + p.kv_pos[m]) * p.kv_dl;
+          if (n < 2 * p.kv_dl) p.kc[slot + (n - p.kv_dl)] = f;
+          else p.vc[slot + (n - 2 * p.kv_dl)] = f;
+        }
+      } else if (KIND == OUT_F16) {
+        reinterpret_cast<__half*>(p.out)[o] = __float2half_rn(f);
+      } else {
+        reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(f);
+      }
     }
   }
   cluster_sync();  // peers may still be reading this CTA's partial
@@ -1823,6 +1839,33 @@ int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float s
   const int kind = out_type == ZQ_OUT_F32 ? OUT_F32 : out_type == ZQ_OUT_F16 ? OUT_F16 : OUT_BF16;
   return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, kind, p,
                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                 int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                 float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
+                 int64_t max_ctx, void* stream) {
+  ZQ_CHECK_ARG(w_row_scales != nullptr && kcache && vcache && pos, ZQ_ERR_USAGE, "linear + kv append needs every operand");
+  ZQ_CHECK_ARG(N == 3LL * dmodel_local && ld_out >= N, ZQ_ERR_SHAPE, "qkv output must be 3 x dmodel_local wide");
+  static int skinny_mode = -1;
+  if (skinny_mode < 0) {
+    const char* e = getenv("ZQ_GEMM_SKINNY");
+    skinny_mode = e ? atoi(e) : 1;
+  }
+  if (M > 64 || skinny_mode == 0) return ZQ_ERR_UNSUPPORTED;  // prefill: linear, then zq_kv_append
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.out = out;
+  p.ld_out = ld_out;
+  p.token_scales = token_scales;
+  p.row_scales = w_row_scales;
+  p.bias = bias;
+  p.kc = kcache;
+  p.vc = vcache;
+  p.kv_pos = pos;
+  p.kv_dl = dmodel_local;
+  p.kv_max_ctx = max_ctx;
+  return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, OUT_F32, p, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int zq_linear_ln_quantize(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq,

@@ -150,6 +150,17 @@ class DecoderEngine:
                w.row_scales().data_ptr(), N.ptr(bias) if bias_on else None, t, w.rows, k,
                out.data_ptr(), out.stride(0), N.OUT_F32, N.stream_ptr())
 
+    def _qkv_kv(self, xq, sx, blk, qkv, li: int, t: int) -> bool:
+        """Decode step: QKV linear with the KV-cache append in its epilogue
+        (zq_linear_kv); False when unsupported (the caller appends separately)."""
+        w = blk.w_qkv
+        wp, ldw, wb = w.weight_operand()
+        rc = N.call_rc("zq_linear_kv", xq.data_ptr(), xq.stride(0), sx.data_ptr(), wp, ldw, wb,
+                       w.row_scales().data_ptr(), blk.b_qkv.data_ptr(), t, w.rows, xq.shape[1], qkv.data_ptr(),
+                       qkv.stride(0), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(), self.pos.data_ptr(),
+                       self.dl, self.max_ctx, N.stream_ptr())
+        return rc != N.ZQ_ERR_UNSUPPORTED
+
     def _tok_quant(self, x, q, s):
         t, d = x.shape
         N.call("zq_quantize_tokenwise", x.data_ptr(), t, d, x.stride(0), 8, q.data_ptr(), q.stride(0),
@@ -192,10 +203,11 @@ class DecoderEngine:
         x, xq, sx = B["x"], B["xq"], B["sx"]
         for li, blk in enumerate(self.blocks):
             qkv = B["qkv"]
-            self._linear(xq, sx, blk.w_qkv, blk.b_qkv, qkv)
-            N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), self.batch, rows_per_seq, dl,
-                   self.pos.data_ptr(), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(),
-                   self.max_ctx, N.stream_ptr())
+            if prefill or not self._qkv_kv(xq, sx, blk, qkv, li, t):
+                self._linear(xq, sx, blk.w_qkv, blk.b_qkv, qkv)
+                N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), self.batch, rows_per_seq, dl,
+                       self.pos.data_ptr(), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(),
+                       self.max_ctx, N.stream_ptr())
             if prefill:
                 attention(qkv[:, :dl], qkv[:, dl:2 * dl], qkv[:, 2 * dl:], self.hl, True, self.batch,
                           out=B["ctx"])
