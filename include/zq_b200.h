@@ -156,7 +156,7 @@ int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t 
  * each), ctx [batch*seq, ld_ctx].  head_dim 64: tcgen05 (seq <= 128: kind::f16
  * with a two-term hi/lo split of power-of-two-scaled tiles; longer: kind::tf32
  * 3-term split with an online softmax), ~fp32 accuracy (tolerance parity).
- * Other head_dim (multiples of 32 up to 256): CUDA-core fp32 flash attention.
+ * Other head_dim (multiples of 16 up to 256): CUDA-core fp32 flash attention.
  * Returns ZQ_ERR_UNSUPPORTED otherwise. */
 int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads,
                      int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,

@@ -810,7 +810,7 @@ template <int DH>
 __global__ void __launch_bounds__(128)
     attention_general_kernel(const float* __restrict__ qkv, int64_t ld_qkv, int seq, int heads, int causal,
                              float scale, float* __restrict__ ctx, int64_t ld_ctx) {
-  constexpr int NJ = DH / 32;   // head-dim columns per lane
+  constexpr int NJ = (DH + 31) / 32;  // head-dim columns per lane (the last one masked if DH % 32)
   constexpr int RW = 8;         // query rows per warp
   constexpr int QB = 4 * RW;    // query rows per CTA
   constexpr int KP = DH + 4;    // padded K row (16-byte loads stay conflict-free)
@@ -899,6 +899,7 @@ __global__ void __launch_bounds__(128)
       for (int r = 0; r < RW; ++r) pk[r] = __shfl_sync(0xffffffffu, p[r], kk);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
+        if (DH % 32 != 0 && lane + 32 * j >= DH) continue;
         const float vv = sV[kk * DH + lane + 32 * j];
 #pragma unroll
         for (int r = 0; r < RW; ++r) o[r][j] = __fmaf_rn(pk[r], vv, o[r][j]);
@@ -912,7 +913,8 @@ __global__ void __launch_bounds__(128)
     const float inv = __frcp_rn(l[r]);
     float* dst = ctx + ((int64_t)b * seq + q) * ld_ctx + h * DH;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) dst[lane + 32 * j] = __fmul_rn(o[r][j], inv);
+    for (int j = 0; j < NJ; ++j)
+      if (DH % 32 == 0 || lane + 32 * j < DH) dst[lane + 32 * j] = __fmul_rn(o[r][j], inv);
   }
 }
 
@@ -1237,18 +1239,25 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
                    (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                ZQ_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
   if (head_dim != kAttD) {  // CUDA-core flash attention for the other head sizes
-    ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
-                 "attention supports head_dim 64 (tensor cores) or a multiple of 32 up to 256");
+    ZQ_CHECK_ARG(head_dim % 16 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
+                 "attention supports head_dim 64 (tensor cores) or a multiple of 16 up to 256");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e2;
     switch (head_dim) {
+      case 16: e2 = launch_att_general<16>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 32: e2 = launch_att_general<32>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 48: e2 = launch_att_general<48>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 80: e2 = launch_att_general<80>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 112: e2 = launch_att_general<112>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 96: e2 = launch_att_general<96>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 128: e2 = launch_att_general<128>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 160: e2 = launch_att_general<160>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 192: e2 = launch_att_general<192>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
       case 224: e2 = launch_att_general<224>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
-      default: e2 = launch_att_general<256>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      case 256: e2 = launch_att_general<256>(qkv, ld_qkv, batch, seq, heads, causal, scale, ctx, ld_ctx, st); break;
+      default:
+        set_error("attention: head_dim %d has no instantiation", head_dim);
+        return ZQ_ERR_UNSUPPORTED;
     }
     if (e2 != cudaSuccess) {
       set_error("attention launch: %s", cudaGetErrorString(e2));

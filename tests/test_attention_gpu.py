@@ -39,7 +39,7 @@ def test_fused_attention_close_to_f64(seq, causal):
     assert rel < tol and err < 1e-4, (rel, err)
 
 
-@pytest.mark.parametrize("dh,heads,seq", [(256, 4, 128), (96, 8, 128), (96, 4, 77), (32, 6, 40), (128, 2, 300),
+@pytest.mark.parametrize("dh,heads,seq", [(256, 4, 128), (96, 8, 128), (96, 4, 77), (32, 6, 40), (128, 2, 300), (16, 4, 33), (48, 3, 50),
                                           (256, 2, 1)])
 @pytest.mark.parametrize("causal", [True, False])
 def test_general_head_dim_attention_close_to_f64(dh, heads, seq, causal):
