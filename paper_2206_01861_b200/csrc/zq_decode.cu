@@ -218,12 +218,11 @@ __global__ void __launch_bounds__(THREADS) decode_attention_kernel(
 // The embedding streams from HBM once per step at up to the copy rate; the split
 // costs ~4 FP32 ops per weight element on otherwise idle CUDA cores.
 // ---------------------------------------------------------------------------
-constexpr int kLmRows = 128, kLmK = 64, kLmS1 = 4, kLmS2 = 2, kLmTok = 16;
-constexpr int kLmF32Stage = kLmRows * kLmK * 4;      // 32 KB: two [128 x 32] f32 boxes
-constexpr int kLmOpE = kLmRows * kLmK * 2;           // 16 KB f16 tile
-constexpr int kLmOpX = kLmTok * kLmK * 2;            // 2 KB
-constexpr int kLmOpStage = 2 * kLmOpE + 2 * kLmOpX;  // 36 KB
-constexpr int kLmSmem = kLmS1 * kLmF32Stage + kLmS2 * kLmOpStage + 256;
+constexpr int kLmRows = 128, kLmK = 64, kLmS = 6, kLmTok = 16;
+constexpr int kLmE = kLmRows * kLmK * 4;          // 32 KB: two [128 x 32] f32 boxes, converted in place
+constexpr int kLmX = kLmTok * kLmK * 2;           // 2 KB f16 token tile
+constexpr int kLmStage = kLmE + 2 * kLmX;         // 36 KB
+constexpr int kLmSmem = kLmS * kLmStage + 256;
 
 __device__ __forceinline__ float lm_pow2_scale(uint32_t max_bits) {  // max * f in [2^14, 2^15)
   const int E = (int)((max_bits >> 23) & 0xFF);
@@ -289,16 +288,17 @@ __global__ void __launch_bounds__(192, 1)
     lm_head_kernel(const __grid_constant__ CUtensorMap tmE, const __half* __restrict__ xh,
                    const __half* __restrict__ xl, const float* __restrict__ xinv, int ntok, int64_t vocab,
                    int dim, float fe, float inv_fe, unsigned long long* __restrict__ keys) {
+  // Each stage: the two f32 boxes of a [128 x 64] embedding k-block, which the
+  // converter thread of row r rewrites in place (row r only): box 0 row r <- the
+  // 64 f16 hi values, box 1 row r <- the 64 f16 lo values, i.e. two K-major
+  // SWIZZLE_128B f16 tiles; plus the tokens' f16 hi / lo k-block.
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sF = smem;                                 // [S1] f32 stages
-  uint8_t* sO = smem + kLmS1 * kLmF32Stage;           // [S2] {Eh, El, Xh, Xl}
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + kLmS2 * kLmOpStage);
-  uint64_t* f_full = bars;                  // [S1]
-  uint64_t* f_empty = bars + kLmS1;         // [S1]
-  uint64_t* o_full = bars + 2 * kLmS1;      // [S2]
-  uint64_t* o_empty = o_full + kLmS2;       // [S2]
-  uint64_t* t_full = o_empty + kLmS2;       // [2]
-  uint64_t* t_empty = t_full + 2;           // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLmS * kLmStage);
+  uint64_t* e_full = bars;             // [S] TMA bytes landed
+  uint64_t* c_full = bars + kLmS;      // [S] converted (4 warps)
+  uint64_t* s_empty = bars + 2 * kLmS; // [S] MMAs done with the stage
+  uint64_t* t_full = bars + 3 * kLmS;  // [2]
+  uint64_t* t_empty = t_full + 2;      // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (int)((vocab + kLmRows - 1) / kLmRows);
@@ -306,8 +306,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();
     prefetch_tmap(&tmE);
-    for (int i = 0; i < kLmS1; ++i) mbar_init(&f_full[i], 1), mbar_init(&f_empty[i], 4);
-    for (int i = 0; i < kLmS2; ++i) mbar_init(&o_full[i], 4), mbar_init(&o_empty[i], 1);
+    for (int i = 0; i < kLmS; ++i) mbar_init(&e_full[i], 1), mbar_init(&c_full[i], 4), mbar_init(&s_empty[i], 1);
     for (int i = 0; i < 2; ++i) mbar_init(&t_full[i], 1), mbar_init(&t_empty[i], 4);
     fence_barrier_init();
   }
@@ -318,21 +317,18 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tslot;
   pdl_trigger();
   if (warp == 0) {
-    // ---- TMA producer: f32 embedding k-blocks (the weights do not depend on the
-    // previous kernel: the first stages go out before the grid dependency) ----
+    // ---- TMA producer (the embedding does not depend on the previous kernel) ----
     int st = 0, ph = 0;
-    bool waited = false;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&f_empty[st], ph ^ 1);
+        mbar_wait(&s_empty[st], ph ^ 1);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&f_full[st], kLmF32Stage);
-          tma_load_2d(sF + st * kLmF32Stage, &tmE, &f_full[st], kb * kLmK, tile * kLmRows);
-          tma_load_2d(sF + st * kLmF32Stage + kLmF32Stage / 2, &tmE, &f_full[st], kb * kLmK + 32, tile * kLmRows);
+          mbar_arrive_expect_tx(&e_full[st], kLmE);
+          tma_load_2d(smem + st * kLmStage, &tmE, &e_full[st], kb * kLmK, tile * kLmRows);
+          tma_load_2d(smem + st * kLmStage + kLmE / 2, &tmE, &e_full[st], kb * kLmK + 32, tile * kLmRows);
         }
         __syncwarp();
-        if (++st == kLmS1) st = 0, ph ^= 1;
-        (void)waited;
+        if (++st == kLmS) st = 0, ph ^= 1;
       }
   } else if (warp == 1) {
     // ---- MMA issuer ----
@@ -343,23 +339,23 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&t_empty[acc], aph ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&o_full[st], ph);
+        mbar_wait(&c_full[st], ph);
         tc_fence_after();
         if (lane == 0) {
-          uint8_t* o = sO + st * kLmOpStage;
-          const uint64_t dEh = make_sw128_desc(smem_u32(o)), dEl = make_sw128_desc(smem_u32(o + kLmOpE));
-          const uint64_t dXh = make_sw128_desc(smem_u32(o + 2 * kLmOpE));
-          const uint64_t dXl = make_sw128_desc(smem_u32(o + 2 * kLmOpE + kLmOpX));
+          uint8_t* o = smem + st * kLmStage;
+          const uint64_t dEh = make_sw128_desc(smem_u32(o)), dEl = make_sw128_desc(smem_u32(o + kLmE / 2));
+          const uint64_t dXh = make_sw128_desc(smem_u32(o + kLmE));
+          const uint64_t dXl = make_sw128_desc(smem_u32(o + kLmE + kLmX));
 #pragma unroll
           for (int t3 = 0; t3 < 3; ++t3)
 #pragma unroll
             for (int ks = 0; ks < kLmK / 16; ++ks)
               mma_f16_ss(tmem + acc * 16, (t3 == 2 ? dEl : dEh) + 2 * ks, (t3 == 1 ? dXl : dXh) + 2 * ks, idesc,
                          (kb | ks | t3) != 0);
-          mma_commit(&o_empty[st]);
+          mma_commit(&s_empty[st]);
         }
         __syncwarp();
-        if (++st == kLmS2) st = 0, ph ^= 1;
+        if (++st == kLmS) st = 0, ph ^= 1;
       }
       if (lane == 0) mma_commit(&t_full[acc]);
       __syncwarp();
@@ -369,43 +365,37 @@ __global__ void __launch_bounds__(192, 1)
     // ---- converters (row r = thread - 64) and epilogue ----
     pdl_wait();
     const int r = threadIdx.x - 64, quarter = warp & 3;
-    int fs = 0, fph = 0, os = 0, oph = 0, acc = 0, aph = 0;
+    int st = 0, ph = 0, acc = 0, aph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&f_full[fs], fph);
-        mbar_wait(&o_empty[os], oph ^ 1);
-        const uint8_t* fsrc = sF + fs * kLmF32Stage;
-        uint8_t* o = sO + os * kLmOpStage;
+        mbar_wait(&e_full[st], ph);
+        uint8_t* o = smem + st * kLmStage;
         uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {  // 16 float4 chunks: box c / 8, chunk c % 8
-          const float4 v = *reinterpret_cast<const float4*>(fsrc + (c >> 3) * (kLmF32Stage / 2) + r * 128 +
+        for (int c = 0; c < 16; ++c) {  // 16 float4 chunks: box c / 8, chunk c % 8 (row r only)
+          const float4 v = *reinterpret_cast<const float4*>(o + (c >> 3) * (kLmE / 2) + r * 128 +
                                                              (((c & 7) ^ (r & 7)) << 4));
           lm_split(__fmul_rn(v.x, fe), __fmul_rn(v.y, fe), hi[2 * c], lo[2 * c]);
           lm_split(__fmul_rn(v.z, fe), __fmul_rn(v.w, fe), hi[2 * c + 1], lo[2 * c + 1]);
         }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // 8 x 16 B per 128-byte f16 row
+        for (int c = 0; c < 8; ++c) {  // row r of box 0 <- hi, of box 1 <- lo (128 B each)
           const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
           *reinterpret_cast<uint4*>(o + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-          *reinterpret_cast<uint4*>(o + kLmOpE + off) =
+          *reinterpret_cast<uint4*>(o + kLmE / 2 + off) =
               make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
         }
         {  // the tokens' f16 k-block: 16 rows x 8 chunks = 128 threads x 16 B each
           const int xr = r >> 3, c = r & 7;
           const uint32_t off = xr * 128 + ((c ^ (xr & 7)) << 4);
           const int64_t src = (int64_t)xr * dim + kb * kLmK + 8 * c;
-          *reinterpret_cast<uint4*>(o + 2 * kLmOpE + off) = *reinterpret_cast<const uint4*>(xh + src);
-          *reinterpret_cast<uint4*>(o + 2 * kLmOpE + kLmOpX + off) = *reinterpret_cast<const uint4*>(xl + src);
+          *reinterpret_cast<uint4*>(o + kLmE + off) = *reinterpret_cast<const uint4*>(xh + src);
+          *reinterpret_cast<uint4*>(o + kLmE + kLmX + off) = *reinterpret_cast<const uint4*>(xl + src);
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&f_empty[fs]);
-          mbar_arrive(&o_full[os]);
-        }
-        if (++fs == kLmS1) fs = 0, fph ^= 1;
-        if (++os == kLmS2) os = 0, oph ^= 1;
+        if (lane == 0) mbar_arrive(&c_full[st]);
+        if (++st == kLmS) st = 0, ph ^= 1;
       }
       // ---- epilogue: 16 logits per vocabulary row -> per-token (max, lowest index) ----
       mbar_wait(&t_full[acc], aph);
