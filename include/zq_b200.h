@@ -189,6 +189,13 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
                             const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
                             void* stream);
 
+/* L2 residency for an engine's hot activation pool: sets the persisting L2
+ * set-aside (min(bytes, device max)) and an access-policy window on `stream`
+ * (persisting hits inside [base, base + bytes), streaming misses).  Call outside
+ * stream capture; kernels captured on the stream carry the window.  bytes == 0
+ * clears the window.  *granted (nullable) receives the set-aside in bytes. */
+int zq_l2_persist(void* stream, const void* base, int64_t bytes, int64_t* granted);
+
 /* Tied LM head + greedy argmax of a decode step (logits = x @ emb^T, argmax per
  * row; float, tolerance parity): x [ntok <= 16, dim] f32 (row stride ld_x),
  * emb [vocab, dim] f32 row-major, emb_scale = a power of two with

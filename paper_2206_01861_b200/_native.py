@@ -50,6 +50,7 @@ _SIGS = {
     "zq_decode_attention_f32": [_p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p, _f32, _p, _i64, _p],
     "zq_linear_kv": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i32, _i64,
                      _p],
+    "zq_l2_persist": [_p, _p, _i64, _p],
     "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
 }
 

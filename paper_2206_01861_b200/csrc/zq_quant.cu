@@ -676,3 +676,43 @@ int zq_layer_norm_quantize(const float* x, const float* residual, const float* g
 }
 
 }  // extern "C"
+
+// L2 residency control for an engine's hot activation pool (cudaStreamAttribute
+// access-policy window, captured into graph kernel nodes): accesses inside
+// [base, base + bytes) are marked persisting (up to the device's set-aside), the
+// rest of the window streaming.  bytes == 0 clears the window.  Returns the
+// persisting set-aside actually granted (bytes) through *granted when non-null.
+extern "C" int zq_l2_persist(void* stream, const void* base, int64_t bytes, int64_t* granted) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  cudaStreamAttrValue attr;
+  memset(&attr, 0, sizeof(attr));
+  int64_t setaside = 0;
+  if (bytes > 0 && max_persist > 0 && max_window > 0) {
+    setaside = bytes < max_persist ? bytes : max_persist;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)setaside) != cudaSuccess) {
+      cudaGetLastError();
+      setaside = 0;
+    }
+  }
+  if (setaside > 0) {
+    const int64_t win = bytes < max_window ? bytes : max_window;
+    attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr.accessPolicyWindow.num_bytes = (size_t)win;
+    attr.accessPolicyWindow.hitRatio = (float)((double)setaside / (double)win > 1.0 ? 1.0 : (double)setaside / (double)win);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  const cudaError_t e = cudaStreamSetAttribute(reinterpret_cast<cudaStream_t>(stream),
+                                               cudaStreamAttributeAccessPolicyWindow, &attr);
+  if (granted) *granted = setaside;
+  if (e != cudaSuccess) {
+    set_error("L2 access policy window: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
