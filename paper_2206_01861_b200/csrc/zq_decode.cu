@@ -529,18 +529,11 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
     if (force >= 1 && force <= 8) C = force;
   }
   const int chunk = (int)((max_ctx + C - 1) / C);
-  static int wide_env = -1;
-  if (wide_env < 0) {
-    const char* ev = getenv("ZQ_DEC_WIDE");
-    wide_env = ev ? atoi(ev) : 0;
-  }
-  const bool wide = wide_env == 1;
   cudaError_t e;
 #define ZQ_DEC(TT, LL, NN, UU)                                                                           \
   e = launch_kernel(decode_attention_kernel<TT, LL, NN, UU>, dim3(batch * heads * C), dim3(TT), 0,      \
                     reinterpret_cast<cudaStream_t>(stream), C, q, ld_q, kcache, vcache, max_ctx, heads,  \
                     head_dim, lens, scale, ctx, ld_ctx, C, chunk)
-  (void)wide;
   const int d4 = head_dim / 4;
   if (d4 <= 8) ZQ_DEC(128, 8, 1, 2);
   else if (d4 <= 16) ZQ_DEC(128, 16, 1, 2);
