@@ -183,11 +183,20 @@ int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, cons
 
 /* One-token-per-sequence attention against the caches (transformer.py:413-440
  * for the last query row): ctx[b, h] = softmax(q.K^T * scale) V over the first
- * lens[b] cached tokens (device int32).  head_dim % 32 == 0, <= 256. */
+ * lens[b] cached tokens (device int32).  head_dim % 32 == 0, <= 256.
+ * `chunks` = context chunks per (sequence, head) merged by the flash-decoding
+ * combine (1, 2, 4 or 8), or 0 for the occupancy rule.  The float result
+ * depends on the chunking, so a tensor-parallel rank passes the count the
+ * unsharded model would use (zq_decode_attention_chunks with the global head
+ * count) to stay bit-identical to one GPU. */
 int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, const float* vcache,
                             int64_t max_ctx, int batch, int heads, int head_dim,
                             const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
-                            void* stream);
+                            int chunks, void* stream);
+
+/* The occupancy rule behind chunks == 0: returns the chunk count for
+ * batch x heads (sequence, head) pairs over a max_ctx cache. */
+int zq_decode_attention_chunks(int batch, int heads, int64_t max_ctx);
 
 /* L2 residency for an engine's hot activation pool: sets the persisting L2
  * set-aside (min(bytes, device max)) and an access-policy window on `stream`

@@ -47,7 +47,8 @@ _SIGS = {
     "zq_gelu_estimate": [_p, _i64, _p, _p, _p],
     "zq_attention_f32": [_p, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _p, _i64, _p],
     "zq_kv_append": [_p, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _p],
-    "zq_decode_attention_f32": [_p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p, _f32, _p, _i64, _p],
+    "zq_decode_attention_f32": [_p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p, _f32, _p, _i64, _i32, _p],
+    "zq_decode_attention_chunks": [_i32, _i32, _i64],
     "zq_linear_kv": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i32, _i64,
                      _p],
     "zq_l2_persist": [_p, _p, _i64, _p],

@@ -922,11 +922,10 @@ template <int DH>
 static cudaError_t launch_att_general(const float* qkv, int64_t ld_qkv, int batch, int seq, int heads, int causal,
                                       float scale, float* ctx, int64_t ld_ctx, cudaStream_t st) {
   const size_t smem = sizeof(float) * (32 * DH + 32 * (DH + 4) + 32 * DH);
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(attention_general_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  });
   return launch_kernel(attention_general_kernel<DH>, dim3((unsigned)((seq + 31) / 32), (unsigned)heads, (unsigned)batch),
                        dim3(128), smem, st, 1, qkv, ld_qkv, seq, heads, causal, scale, ctx, ld_ctx);
 }
@@ -1272,19 +1271,13 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   const int rc = make_tmap_f32(&tm, qkv, (int64_t)batch * seq, 3LL * heads * head_dim, ld_qkv * 4,
                                32, kAttT, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc != ZQ_OK) return rc;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     cudaFuncSetAttribute(attention_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAtt16Smem);
-    attr = true;
-  }
-  int nsm = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  });
+  const int nsm = zq_num_sms();
   const int total = batch * heads;
   cudaError_t e;
   if (seq <= kAttT) {

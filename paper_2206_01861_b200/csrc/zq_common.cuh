@@ -7,7 +7,38 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "zq_b200.h"
+
+// Launcher state is per device: a process may drive several GPUs (and several
+// host threads may launch concurrently).  ZqDeviceOnce runs its body once per
+// device ordinal (idempotent bodies only: two threads may both run it);
+// zq_num_sms() caches the SM count per device.
+struct ZqDeviceOnce {
+  std::atomic<unsigned long long> done{0};
+  template <class F>
+  void operator()(F&& body) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    body(dev);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
+
+static inline int zq_num_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 namespace zq {
 

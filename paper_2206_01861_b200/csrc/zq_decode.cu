@@ -474,22 +474,15 @@ int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, 
   ZQ_CHECK_ARG((reinterpret_cast<uintptr_t>(emb) & 15) == 0 && (reinterpret_cast<uintptr_t>(xh_ws) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(xl_ws) & 15) == 0,
                ZQ_ERR_USAGE, "lm head operands must be 16-byte aligned");
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
+  const int nsm = zq_num_sms();
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CUtensorMap tm;
   int rc = make_tmap_f32(&tm, emb, vocab, dim, dim * 4, 32, kLmRows, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc != ZQ_OK) return rc;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(lm_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmem);
-    attr = true;
-  }
+  });
   // emb_scale: the power of two the caller chose once for the embedding
   const float fe = emb_scale;
   const float inv_fe = 1.0f / emb_scale;
@@ -509,25 +502,24 @@ int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, 
   return ZQ_OK;
 }
 
-int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, const float* vcache,
-                            int64_t max_ctx, int batch, int heads, int head_dim,
-                            const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
-                            void* stream) {
-  ZQ_CHECK_ARG(batch >= 1 && heads >= 1 && max_ctx >= 1, ZQ_ERR_SHAPE, "bad decode attention shape");
-  ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
-               "decode attention supports head_dim % 32 == 0 and <= 256");
+int zq_decode_attention_chunks(int batch, int heads, int64_t max_ctx) {
   // context chunks per (sequence, head): split until ~1000 CTAs of 4 warps are in
   // flight (7 per SM), at most 8 (portable cluster), keeping >= 16 keys per chunk
   int C = 1;
   while (C < 8 && (int64_t)batch * heads * C * 2 <= 7 * 148 && max_ctx / (2 * C) >= 16) C *= 2;
-  {
-    static int force = -1;
-    if (force < 0) {
-      const char* ev = getenv("ZQ_DEC_C");
-      force = ev ? atoi(ev) : 0;
-    }
-    if (force >= 1 && force <= 8) C = force;
-  }
+  return C;
+}
+
+int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, const float* vcache,
+                            int64_t max_ctx, int batch, int heads, int head_dim,
+                            const int32_t* lens, float scale, float* ctx, int64_t ld_ctx,
+                            int chunks, void* stream) {
+  ZQ_CHECK_ARG(batch >= 1 && heads >= 1 && max_ctx >= 1, ZQ_ERR_SHAPE, "bad decode attention shape");
+  ZQ_CHECK_ARG(head_dim % 32 == 0 && head_dim <= 256, ZQ_ERR_UNSUPPORTED,
+               "decode attention supports head_dim % 32 == 0 and <= 256");
+  ZQ_CHECK_ARG(chunks == 0 || chunks == 1 || chunks == 2 || chunks == 4 || chunks == 8, ZQ_ERR_USAGE,
+               "decode attention chunks must be 0 (auto), 1, 2, 4 or 8, got %d", chunks);
+  const int C = chunks ? chunks : zq_decode_attention_chunks(batch, heads, max_ctx);
   const int chunk = (int)((max_ctx + C - 1) / C);
   cudaError_t e;
 #define ZQ_DEC(TT, LL, NN, UU)                                                                           \

@@ -1300,11 +1300,10 @@ template <int BN>
 static int launch_gemm2_ln_t(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, const LnFuseParams& f,
                              int grid, cudaStream_t st) {
   using Cfg = Gemm2Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(zq_gemm2_ln_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
   const cudaError_t e = launch_kernel(zq_gemm2_ln_kernel<BN>, dim3(grid), dim3(Cfg::NUM_THREADS),
                                       Cfg::SMEM_BYTES, st, 1, ta, tb, p, f);
   if (e != cudaSuccess) {
@@ -1444,7 +1443,6 @@ int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols,
   return ZQ_OK;
 }
 
-static int g_num_sms = 0;
 static unsigned long long* g_trace = nullptr;
 static int g_debug = 0;
 
@@ -1452,12 +1450,12 @@ template <int BN, int KIND, int W4>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                          GemmParams p, cudaStream_t st) {
   using Cfg = GemmCfg<BN, W4>;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(zq_gemm_kernel<BN, KIND, W4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
+  const int g_num_sms = zq_num_sms();
   int grid = p.num_tiles < g_num_sms ? p.num_tiles : g_num_sms;
   const cudaError_t e = launch_kernel(zq_gemm_kernel<BN, KIND, W4>, dim3(grid), dim3(Cfg::NUM_THREADS),
                                       Cfg::SMEM_BYTES, st, 1, ta, tb, tc, p);
@@ -1472,16 +1470,19 @@ template <int BN, int KIND, int CL>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, GemmParams p,
                           cudaStream_t st) {
   using Cfg = Gemm2Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(zq_gemm2_kernel<BN, KIND, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
   const int units = (int)((int64_t)(p.num_tiles / p.num_n_tiles) * ((p.num_n_tiles + CL / 2 - 1) / (CL / 2)));
   // co-resident clusters: GPC boundaries can leave fewer than SMs / CL slots
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
+  static std::atomic<int> max_clusters_dev[64];  // per device; 0 = not yet measured
+  const int g_num_sms = zq_num_sms();
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  int max_clusters = max_clusters_dev[dev_ & 63].load(std::memory_order_relaxed);
+  if (max_clusters <= 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * (g_num_sms / CL));
     cfg.blockDim = dim3(Cfg::NUM_THREADS);
@@ -1499,6 +1500,7 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CU
       n = g_num_sms / CL;
     }
     max_clusters = n < g_num_sms / CL ? n : g_num_sms / CL;
+    max_clusters_dev[dev_ & 63].store(max_clusters, std::memory_order_relaxed);
     if (getenv("ZQ_GEMM_DEBUG")) fprintf(stderr, "[zq] gemm2 BN=%d CL=%d: %d co-resident clusters\n", BN, CL, max_clusters);
   }
   const int clusters = units < max_clusters ? units : max_clusters;
@@ -1529,7 +1531,7 @@ static int pick_bn(int64_t M, int64_t N) {
   for (int i = 0; i < 3; ++i) {
     int bn = cands[i];
     int64_t tiles = mt * ((N + bn - 1) / bn);
-    if (tiles >= g_num_sms || bn == 64) {
+    if (tiles >= zq_num_sms() || bn == 64) {
       if (bn > N && bn > 64) continue;
       return bn;
     }
@@ -1541,12 +1543,11 @@ template <int MP, int KIND, int W4>
 static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmParams p, int S,
                            cudaStream_t st) {
   using Cfg = SkinnyCfg<MP, W4>;
-  static bool attr = false;
-  if (!attr) {
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
     cudaFuncSetAttribute(zq_gemm_skinny_kernel<MP, KIND, W4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
   cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND, W4>, dim3(p.num_n_tiles * S), dim3(128),
                                 Cfg::SMEM_BYTES, st, S, tw, tx, p, S);
   if (e != cudaSuccess) {
@@ -1567,7 +1568,7 @@ static int pick_split(int n_tiles, int nkb) {
   // S (clusters of 3 / 6 co-schedule poorly) or filling two CTAs per SM never beat
   // this rule, tools/microbench.py skinny)
   int S = 1;
-  while (S < 8 && n_tiles * S * 2 <= 2 * g_num_sms * ZQ_SKINNY_CTAS_PER_SM && nkb / (2 * S) >= 2) S *= 2;
+  while (S < 8 && n_tiles * S * 2 <= 2 * zq_num_sms() * ZQ_SKINNY_CTAS_PER_SM && nkb / (2 * S) >= 2) S *= 2;
   return S;
 }
 
@@ -1623,12 +1624,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
     set_error("cuTensorMapEncodeTiled unavailable");
     return ZQ_ERR_CUDA;
   }
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+  const int g_num_sms = zq_num_sms();
   // decode-sized token counts: weight-streaming skinny kernel (ZQ_GEMM_SKINNY=0 disables)
   static int skinny_mode = -1;
   if (skinny_mode < 0) {
@@ -1889,12 +1885,7 @@ int zq_linear_ln_quantize(const int8_t* xq, int64_t ld_x, const float* token_sca
   const int BN = (int)(2 * L);
   const int NT = (int)(N / BN);
   if ((NT & (NT - 1)) != 0 || NT > 64) return ZQ_ERR_UNSUPPORTED;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+  const int g_num_sms = zq_num_sms();
   const int npairs = g_num_sms / 2;
   if (NT > npairs) return ZQ_ERR_UNSUPPORTED;
   const int64_t rblocks = (M + 255) / 256;

@@ -662,11 +662,10 @@ int zq_layer_norm_quantize(const float* x, const float* residual, const float* g
     return ZQ_OK;
   }
   size_t smem = sizeof(float) * (cols + 2 * (size_t)plan.nleaves + 2);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static ZqDeviceOnce attr_set_once;
+  attr_set_once([&](int) {
     cudaFuncSetAttribute(ln_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  });
   int threads = cols >= 2048 ? 256 : 128;
   ln_quant_kernel<<<(unsigned)rows, threads, smem, as_stream(stream)>>>(
       x, residual, gamma, beta, cols, eps, qmax_of(bits), plan, ln_out, q, ld_q, token_scales,

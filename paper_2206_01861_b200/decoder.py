@@ -14,11 +14,15 @@ on the caller side:
 * decode attention for one query row per sequence (zq_decode_attention_f32)
   with the context length in device memory, so one decode step is a fixed
   launch sequence captured once in a CUDA graph;
-* the tied LM head (transformer.py:532) and greedy argmax run in float32
-  (torch / cuBLAS: not on the quantized path);
+* the tied LM head (transformer.py:532) and greedy argmax: float32 logits on
+  tcgen05 (zq_lm_head_argmax: two-term f16 split of the final hidden state,
+  fused argmax) for batch <= 16; torch matmul + argmax above that (the head is
+  not on the quantized path);
 * tensor parallelism (tp.py): column-parallel q/k/v/h4h, row-parallel o/4hh
-  with the exact MAX(absmax) + int32 SUM all-reduces, so every rank's result is
-  bit-identical to the single-GPU one.
+  through `tp.row_parallel_linear` (the exact MAX(absmax) + int32 SUM
+  all-reduces), so every rank's result is bit-identical to the single-GPU one.
+  `force_tp=True` takes that route even on one rank (exercises the collectives
+  inside CUDA-graph capture on a 1-GPU box).
 
 Model shapes follow SURVEY.md §8(a): GPT-3 350M (W4/8-A8), GPT-J 6B and
 GPT-NeoX 20B (W8A8); weights are random-init Gaussian(0, 0.02) generated on
@@ -73,12 +77,16 @@ class DecoderEngine:
     `tp=(group, rank, world)` every layer is sharded Megatron-style."""
 
     def __init__(self, cfg: GPTConfig, batch: int, max_ctx: int, seed: int = 0, tp=None,
-                 layers: int | None = None, use_graph: bool = True, blocks=None, embedding=None):
+                 layers: int | None = None, use_graph: bool = True, blocks=None, embedding=None,
+                 force_tp: bool = False):
+        from .tp import CudaOps, ShardedBlock, shard_block
+
         self.cfg = cfg
         self.batch = batch
         self.max_ctx = max_ctx
         self.use_graph = use_graph
         self.group, self.rank, self.world = tp if tp is not None else (None, 0, 1)
+        self._tp = self.world > 1 or force_tp
         nl = cfg.layers if layers is None else layers
         if cfg.heads % self.world or cfg.ffn % self.world:
             raise UsageError(f"{cfg.name}: heads/ffn not divisible by TP degree {self.world}")
@@ -86,14 +94,18 @@ class DecoderEngine:
         self.dl = cfg.dim // self.world               # local attention width
         self.hl = cfg.heads // self.world
         self.fl = cfg.ffn // self.world
-        self.blocks = list(blocks) if blocks is not None else []
-        for i in range(0 if blocks is not None else nl):
-            blk = random_block(cfg.dim, cfg.heads, cfg.mhsa_bits, cfg.ffc_bits, cfg.groups,
-                               seed=seed * 1000 + i, ffn_mult=cfg.ffn // cfg.dim)
-            if self.world > 1:
-                from .tp import CudaOps, shard_block
-
-                blk = shard_block(blk, CudaOps(), self.rank, self.world)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._ops = CudaOps(flag=self.flag, reuse=True)
+        # blocks given by the caller (e.g. checkpoint.load_model) are globally
+        # quantized like generated ones: shard them the same way
+        self.blocks = []
+        src = list(blocks) if blocks is not None else [None] * nl
+        for i, blk in enumerate(src):
+            if blk is None:
+                blk = random_block(cfg.dim, cfg.heads, cfg.mhsa_bits, cfg.ffc_bits, cfg.groups,
+                                   seed=seed * 1000 + i, ffn_mult=cfg.ffn // cfg.dim)
+            if self.world > 1 and not isinstance(blk, ShardedBlock):
+                blk = shard_block(blk, self._ops, self.rank, self.world)
             self.blocks.append(blk)
         nl = len(self.blocks)
         if embedding is not None:
@@ -108,7 +120,7 @@ class DecoderEngine:
         self.vcache = [e(batch, max_ctx, self.dl) for _ in range(nl)]
         self.pos = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.lens = torch.zeros(batch, dtype=torch.int32, device=dev)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.host_pos = None  # host mirror of pos (all sequences advance together)
         self.next_ids = torch.zeros(batch, dtype=torch.int64, device=dev)
         # LM head (zq_lm_head_argmax): one power-of-two scale for the embedding,
         # chosen once, and the per-step f16 split / argmax workspaces
@@ -119,6 +131,9 @@ class DecoderEngine:
                            xl=torch.zeros(16 * cfg.dim, dtype=torch.float16, device=dev),
                            xinv=torch.zeros(16, dtype=torch.float32, device=dev),
                            keys=torch.zeros(16, dtype=torch.int64, device=dev))
+        # decode-attention context chunking planned for the UNSHARDED head count:
+        # the float merge order then does not depend on the TP degree
+        self._dec_chunks = int(N.load().zq_decode_attention_chunks(batch, cfg.heads, max_ctx))
         self._bufs: dict[int, dict] = {}
         self._graph = None
         self.scale = float(np.float32(1.0 / math.sqrt(cfg.head_dim)))
@@ -135,8 +150,7 @@ class DecoderEngine:
                 x=e(t, d), h=e(t, d), qkv=e(t, 3 * dl), ctx=e(t, dl), attn=e(t, d), u=e(t, fl),
                 z=e(t, fl), f=e(t, d), out=e(t, d),
                 xq=quant.padded_int8(t, d), cq=quant.padded_int8(t, dl), hq=quant.padded_int8(t, d),
-                zq=quant.padded_int8(t, fl), sx=e(t), sc=e(t), sh=e(t), sz=e(t), amax=e(t),
-                acc=torch.empty((t, d), dtype=torch.int32, device=dev),
+                zq=quant.padded_int8(t, fl), sx=e(t), sc=e(t), sh=e(t), sz=e(t),
                 last=e(self.batch, d), lq=quant.padded_int8(self.batch, d), ls=e(self.batch),
                 logits=e(self.batch, self.cfg.vocab),
             )
@@ -173,29 +187,16 @@ class DecoderEngine:
                self.flag.data_ptr(), N.stream_ptr())
 
     def _row_parallel(self, x, B, w, bias, out, xq, xs):
-        """o / 4hh projection: local (world 1) or Megatron row-parallel with the
-        exact MAX(absmax) + int32 SUM all-reduces (tp.py steps 1-5)."""
-        import torch.distributed as dist
-
-        if self.world == 1:
+        """o / 4hh projection: local fused linear (one rank), or Megatron
+        row-parallel through tp.row_parallel_linear (the exact MAX(absmax) +
+        int32 SUM all-reduces, tp.py steps 1-5)."""
+        if not self._tp:
             self._tok_quant(x, xq, xs)
             self._linear(xq, xs, w, bias, out)
             return
-        t, k = x.shape
-        amax = B["amax"][:t]
-        N.call("zq_row_absmax", x.data_ptr(), t, k, x.stride(0), amax.data_ptr(), self.flag.data_ptr(),
-               N.stream_ptr())
-        dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=self.group)
-        N.call("zq_quantize_with_absmax", x.data_ptr(), t, k, x.stride(0), amax.data_ptr(), 8,
-               xq.data_ptr(), xq.stride(0), xs.data_ptr(), N.stream_ptr())
-        acc = B["acc"][:t]
-        wp, ldw, wb = w.weight_operand()
-        N.call("zq_igemm_s32", xq.data_ptr(), xq.stride(0), wp, ldw, wb, t, w.rows, k, acc.data_ptr(),
-               acc.stride(0), N.stream_ptr())
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
-        N.call("zq_dequant_epilogue", acc.data_ptr(), acc.stride(0), xs.data_ptr(), 0.0,
-               w.row_scales().data_ptr(), bias.data_ptr(), t, w.rows, out.data_ptr(), out.stride(0),
-               N.OUT_F32, N.stream_ptr())
+        from .tp import row_parallel_linear
+
+        row_parallel_linear(self._ops, x, w, bias, self.group, out=out)
 
     def _layers(self, B, t: int, rows_per_seq: int, prefill: bool):
         """All blocks over B['x'] (t = batch * rows_per_seq rows); y -> B['x']."""
@@ -215,13 +216,13 @@ class DecoderEngine:
                 N.call("zq_decode_attention_f32", qkv.data_ptr(), qkv.stride(0), self.kcache[li].data_ptr(),
                        self.vcache[li].data_ptr(), self.max_ctx, self.batch, self.hl, self.cfg.head_dim,
                        self.lens.data_ptr(), self.scale, B["ctx"].data_ptr(), B["ctx"].stride(0),
-                       N.stream_ptr())
+                       self._dec_chunks, N.stream_ptr())
             ln1 = blk.ln1 if hasattr(blk, "ln1") else (blk.ln1_gamma, blk.ln1_beta)
             ln2 = blk.ln2 if hasattr(blk, "ln2") else (blk.ln2_gamma, blk.ln2_beta)
             self._row_parallel(B["ctx"], B, blk.w_o, blk.b_o, B["attn"], B["cq"], B["sc"])
             self._ln_quant(x, B["attn"], ln1[0], ln1[1], B["h"], B["hq"], B["sh"])
             self._linear(B["hq"], B["sh"], blk.w_h4h, blk.b_h4h, B["u"])
-            if self.world == 1:
+            if not self._tp:
                 u = B["u"]
                 N.call("zq_gelu_quantize", u.data_ptr(), t, self.fl, self.fl, 8, None, B["zq"].data_ptr(),
                        B["zq"].stride(0), B["sz"].data_ptr(), self.flag.data_ptr(), N.stream_ptr())
@@ -266,11 +267,13 @@ class DecoderEngine:
         t = self.batch * T
         B = self._buffers(t)
         B["ids"].copy_(ids.reshape(-1), non_blocking=True)
+        self.flag.zero_()
         self.pos.zero_()
         self._embed(B, B["ids"])
         self._layers(B, t, T, prefill=True)
         self._head(B, t, T)
         self.pos.fill_(T)
+        self.host_pos = T
         return self.next_ids
 
     def _step_launches(self):
@@ -282,31 +285,51 @@ class DecoderEngine:
         self.pos.add_(1)
 
     def capture(self):
+        """Capture one decode step into a CUDA graph.  The eager warm-up before
+        the capture really runs a step (it advances pos, overwrites next_ids
+        with the following token and writes K/V at pos); every piece of decode
+        state it touches is restored afterwards, so the first replay computes
+        exactly the step an eager call would have."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        saved = self.pos.clone()
+        saved = (self.pos.clone(), self.lens.clone(), self.next_ids.clone())
+
+        def restore():
+            self.pos.copy_(saved[0])
+            self.lens.copy_(saved[1])
+            self.next_ids.copy_(saved[2])
+
         with torch.cuda.stream(s):
             self._step_launches()
         torch.cuda.current_stream().wait_stream(s)
-        self.pos.copy_(saved)
+        restore()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self._step_launches()
-        self.pos.copy_(saved)
+        restore()
         self._graph = g
 
     def step(self) -> torch.Tensor:
-        """Generate one token per sequence (next_ids is updated in place)."""
+        """Generate one token per sequence (next_ids is updated in place).
+        Raises UsageError before the key/value cache would overflow max_ctx."""
+        if self.host_pos is None:
+            raise UsageError("step() before prefill()")
+        if self.host_pos >= self.max_ctx:
+            raise UsageError(f"decode position {self.host_pos} is past max_ctx {self.max_ctx}")
         if self.use_graph:
             if self._graph is None:
                 self.capture()
             self._graph.replay()
         else:
             self._step_launches()
+        self.host_pos += 1
         return self.next_ids
 
     def generate(self, ids, new_tokens: int) -> torch.Tensor:
+        T = (ids.shape if isinstance(ids, torch.Tensor) else np.asarray(ids).shape)[-1]
+        if new_tokens < 1 or T + new_tokens - 1 > self.max_ctx:
+            raise UsageError(f"{T} prompt + {new_tokens} new tokens do not fit max_ctx {self.max_ctx}")
         out = [self.prefill(ids).clone()]
         for _ in range(new_tokens - 1):
             out.append(self.step().clone())

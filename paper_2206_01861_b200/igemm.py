@@ -70,8 +70,9 @@ def check_overflow_guard(inner_dim: int, act_bits: int, weight_bits: int) -> Non
         )
 
 
-def igemm(xq: QuantizedActivation, wq: QuantizedMatrix) -> IntAccumulator:
-    """igemm.py:66-80: acc[i][j] = sum_p xq[i][p] * wq[j][p], exact int32."""
+def igemm(xq: QuantizedActivation, wq: QuantizedMatrix, out: torch.Tensor | None = None) -> IntAccumulator:
+    """igemm.py:66-80: acc[i][j] = sum_p xq[i][p] * wq[j][p], exact int32.
+    `out` (B200 extension): a caller-owned int32 [tokens, n] destination."""
     if xq.values.shape[1] != wq.cols:
         raise ShapeError(
             f"igemm inner dimensions differ: activation {tuple(xq.values.shape)} vs weight "
@@ -81,7 +82,11 @@ def igemm(xq: QuantizedActivation, wq: QuantizedMatrix) -> IntAccumulator:
     a = xq.gemm_operand()
     m, k = a.shape
     n = wq.rows
-    acc = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    elif out.dtype != torch.int32 or tuple(out.shape) != (m, n) or out.stride(1) != 1:
+        raise ShapeError(f"igemm out must be int32 {(m, n)} with unit column stride")
+    acc = out
     wp, ld_w, wb = wq.weight_operand()
     N.call("zq_igemm_s32", a.data_ptr(), a.stride(0), wp, ld_w, wb, m, n, k, acc.data_ptr(),
            acc.stride(0), N.stream_ptr())
@@ -103,18 +108,22 @@ def _act_scale_args(act_scales, tokens: int):
 
 
 def dequant_epilogue(acc: IntAccumulator, act_scales, w: QuantizedMatrix, bias=None,
-                     out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
-    """igemm.py:83-112: out = acc * act_scale(i) * group_scale(group_of(j)) + bias[j]."""
+                     out_dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None) -> torch.Tensor:
+    """igemm.py:83-112: out = acc * act_scale(i) * group_scale(group_of(j)) + bias[j].
+    `out` (B200 extension): caller-owned destination (its dtype wins)."""
     a = acc.acc
     m, n = a.shape
     if w.rows != n:
         raise ShapeError(f"epilogue weight rows {w.rows} != accumulator cols {n}")
     ts_ptr, sscale, _keep = _act_scale_args(act_scales, m)
     b = None if bias is None else as_device_f32(bias).reshape(-1)
-    out = torch.empty((m, n), dtype=out_dtype, device=a.device)
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=a.device)
+    elif tuple(out.shape) != (m, n) or out.stride(1) != 1 or out.dtype not in _OUT_CODES:
+        raise ShapeError(f"epilogue out must be {(m, n)} float32/float16/bfloat16 with unit column stride")
     N.call("zq_dequant_epilogue", a.data_ptr(), a.stride(0), ts_ptr, sscale,
            w.row_scales().data_ptr(), N.ptr(b), m, n, out.data_ptr(), out.stride(0),
-           _OUT_CODES[out_dtype], N.stream_ptr())
+           _OUT_CODES[out.dtype], N.stream_ptr())
     return out
 
 

@@ -79,14 +79,17 @@ def shard_block(block, ops, rank: int, world: int) -> ShardedBlock:
         heads_local=hl, dim=d)
 
 
-def _row_parallel_linear(ops, x_local, w_local, bias, group):
-    """Steps 1-5 above for one row-parallel projection."""
+def row_parallel_linear(ops, x_local, w_local, bias, group, out=None):
+    """Steps 1-5 above for one row-parallel projection.  This is the one
+    implementation: `tp_block_forward` and `decoder.DecoderEngine` (world > 1,
+    or `force_tp`) both call it.  `out` (optional) receives the epilogue."""
     amax = ops.row_absmax(x_local)
     dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=group)
     xq, scales = ops.quantize_with_absmax(x_local, amax)
     acc = ops.igemm_s32(xq, w_local)
     dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    return ops.epilogue(acc, scales, w_local, bias)
+    return ops.epilogue(acc, scales, w_local, bias, out=out)
+
 
 
 def tp_block_forward(x, sb: ShardedBlock, ops, causal: bool, group=None, batch: int = 1):
@@ -96,11 +99,11 @@ def tp_block_forward(x, sb: ShardedBlock, ops, causal: bool, group=None, batch: 
     qkv = ops.linear(xq, xs, sb.w_qkv, sb.b_qkv)          # column-parallel, no comm
     dl = ops.cols(qkv) // 3
     ctx = ops.attention(qkv, dl, sb.heads_local, causal, batch)
-    attn_out = _row_parallel_linear(ops, ctx, sb.w_o, sb.b_o, group)
+    attn_out = row_parallel_linear(ops, ctx, sb.w_o, sb.b_o, group)
     h, hq, hs = ops.ln_quant(x, attn_out, *sb.ln1)
     u = ops.linear(hq, hs, sb.w_h4h, sb.b_h4h)              # column-parallel
     z = ops.gelu(u)                                          # exact float GeLU, local columns
-    f = _row_parallel_linear(ops, z, sb.w_4hh, sb.b_4hh, group)
+    f = row_parallel_linear(ops, z, sb.w_4hh, sb.b_4hh, group)
     y, _, _ = ops.ln_quant(h, f, *sb.ln2)
     return y
 
@@ -111,13 +114,31 @@ def tp_block_forward(x, sb: ShardedBlock, ops, causal: bool, group=None, batch: 
 
 
 class CudaOps:
-    """`ops` implementation over libzq_b200 (device tensors)."""
+    """`ops` implementation over libzq_b200 (device tensors).
 
-    def __init__(self):
+    `flag` (an int32 device tensor) collects non-finite detections; by default
+    a private one.  With `reuse=True` the row-parallel workspaces (absmax,
+    int8 slice, token scales, int32 partials) are kept per (rows, cols) and
+    reused, so a decode step issues no allocations (CUDA-graph friendly)."""
+
+    def __init__(self, flag=None, reuse: bool = False):
         from . import _native, igemm, quant
 
         self.N, self.igemm, self.quant = _native, igemm, quant
-        self.flag = quant.FiniteFlag()
+        if flag is None:
+            self.flag = quant.FiniteFlag()
+        else:
+            self.flag = quant.FiniteFlag.__new__(quant.FiniteFlag)
+            self.flag.t = flag
+        self.reuse = reuse
+        self._ws: dict = {}
+
+    def _buf(self, key, make):
+        if not self.reuse:
+            return make()
+        if key not in self._ws:
+            self._ws[key] = make()
+        return self._ws[key]
 
     # --- weight container plumbing ---
     @staticmethod
@@ -169,24 +190,27 @@ class CudaOps:
 
     def row_absmax(self, x):
         t, d = x.shape
-        out = torch.empty(t, dtype=torch.float32, device=x.device)
+        out = self._buf(("amax", t, d), lambda: torch.empty(t, dtype=torch.float32, device=x.device))
         self.N.call("zq_row_absmax", x.data_ptr(), t, d, x.stride(0), out.data_ptr(), self.flag.ptr,
                     self.N.stream_ptr())
         return out
 
     def quantize_with_absmax(self, x, amax):
         t, d = x.shape
-        q = self.quant.padded_int8(t, d)
-        s = torch.empty(t, dtype=torch.float32, device=x.device)
+        q = self._buf(("q", t, d), lambda: self.quant.padded_int8(t, d))
+        s = self._buf(("s", t, d), lambda: torch.empty(t, dtype=torch.float32, device=x.device))
         self.N.call("zq_quantize_with_absmax", x.data_ptr(), t, d, x.stride(0), amax.data_ptr(), 8,
                     q.data_ptr(), q.stride(0), s.data_ptr(), self.N.stream_ptr())
         return self.quant.QuantizedActivation(values=q, bits=8, token_scales=s), s
 
     def igemm_s32(self, xq, w):
-        return self.igemm.igemm(xq, w).acc
+        t = xq.values.shape[0]
+        acc = self._buf(("acc", t, w.rows), lambda: torch.empty((t, w.rows), dtype=torch.int32,
+                                                                device=xq.values.device))
+        return self.igemm.igemm(xq, w, out=acc).acc
 
-    def epilogue(self, acc, scales, w, bias):
-        return self.igemm.dequant_epilogue(self.igemm.IntAccumulator(acc), scales, w, bias)
+    def epilogue(self, acc, scales, w, bias, out=None):
+        return self.igemm.dequant_epilogue(self.igemm.IntAccumulator(acc), scales, w, bias, out=out)
 
     def ln_quant(self, x, res, gamma, beta):
         y = torch.empty_like(x)
@@ -207,4 +231,4 @@ def init_from_env(backend: str = "nccl"):
     return dist.get_rank(), dist.get_world_size()
 
 
-__all__ = ["ShardedBlock", "shard_block", "tp_block_forward", "CudaOps", "init_from_env"]
+__all__ = ["ShardedBlock", "shard_block", "row_parallel_linear", "tp_block_forward", "CudaOps", "init_from_env"]

@@ -222,14 +222,14 @@ def quantize_block(block, precision: PrecisionConfig) -> DeviceBlock:
 
 
 def random_block(dim: int, num_heads: int, mhsa_bits: int, ffc_bits: int, groups: int,
-                 seed: int = 0, ffn_mult: int = 4) -> DeviceBlock:
+                 seed: int = 0, ffn_mult: int = 4, std: float = INIT_STD) -> DeviceBlock:
     """Random-init block generated and quantized on device (Gaussian(0, 0.02)
     weights, zero biases, identity LN — transformer.py:261-297's recipe, with a
     device RNG so GPT-scale layers don't need a host round trip)."""
     gen = torch.Generator(device="cuda").manual_seed(seed)
 
     def w(r, c):
-        return torch.randn((r, c), generator=gen, device="cuda") * INIT_STD
+        return torch.randn((r, c), generator=gen, device="cuda") * std
 
     def qm(r, c, bits):
         return quant.quantize_weight_groupwise(w(r, c), min(groups, r), bits)

@@ -93,7 +93,7 @@ def test_decode_attention_vs_torch():
         ctx = torch.empty(batch, dl, device="cuda")
         scale = 1.0 / dh ** 0.5
         N.call("zq_decode_attention_f32", q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), max_ctx,
-               batch, heads, dh, lens.data_ptr(), scale, ctx.data_ptr(), ctx.stride(0), N.stream_ptr())
+               batch, heads, dh, lens.data_ptr(), scale, ctx.data_ptr(), ctx.stride(0), 0, N.stream_ptr())
         for b in range(batch):
             n = int(lens[b])
             qh = q[b, :dl].double().view(heads, 1, dh)
@@ -133,3 +133,62 @@ def test_lm_head_argmax_vs_f64():
             gap = float(top2.values[t, 0] - top2.values[t, 1])
             if gap > 1e-5 * abs(float(top2.values[t, 0])):
                 assert int(got[t]) == int(ref[t]), (ntok, vocab, t)
+
+
+def test_graph_replay_matches_eager_steps():
+    """The CUDA-graph decode step (use_graph=True, captured on the first step)
+    must produce exactly the eager token stream: the capture's warm-up step
+    may not leak into decode state (next_ids / pos / lens)."""
+    from paper_2206_01861_b200.decoder import DecoderEngine, GPTConfig
+
+    from paper_2206_01861_b200 import transformer as T
+
+    cfg = GPTConfig("tiny-graph", 2, 256, 4, 1024, 512, 8, 8, 16)
+    ids = np.random.default_rng(5).integers(0, cfg.vocab, (4, 7))
+    streams, hidden = [], []
+    for use_graph in (False, True):
+        # weights well above the init scale, so the blocks move the hidden state away
+        # from LN(embedding[last token]) and greedy decoding does not just repeat it
+        blocks = [T.random_block(256, 4, 8, 8, 16, seed=40 + i, std=0.25) for i in range(2)]
+        eng = DecoderEngine(cfg, 4, 20, seed=9, use_graph=use_graph, blocks=blocks)
+        toks = [eng.prefill(ids).cpu().numpy()]
+        hs = []
+        for _ in range(8):
+            toks.append(eng.step().cpu().numpy())
+            hs.append(eng._buffers(4)["out"][:4].cpu().numpy())
+        streams.append(np.stack(toks, 1))
+        hidden.append(np.stack(hs))
+    assert len(np.unique(streams[0])) > 4, streams[0]  # decoding is not a repeat of one token
+    assert np.array_equal(streams[0], streams[1]), (streams[0], streams[1])
+    assert np.array_equal(hidden[0].view(np.uint32), hidden[1].view(np.uint32))
+
+
+def test_decode_bounded_by_max_ctx():
+    from paper_2206_01861_b200.decoder import DecoderEngine, GPTConfig
+    from paper_2206_01861_b200.errors import UsageError
+
+    cfg = GPTConfig("tiny-ctx", 1, 256, 4, 1024, 512, 8, 8, 16)
+    ids = np.random.default_rng(1).integers(0, cfg.vocab, (2, 5))
+    eng = DecoderEngine(cfg, 2, 7, seed=1, use_graph=True)
+    with pytest.raises(UsageError):
+        eng.step()  # before prefill
+    eng.prefill(ids)
+    eng.step()
+    eng.step()  # K/V written at positions 5 and 6 = max_ctx - 1
+    with pytest.raises(UsageError):
+        eng.step()
+    with pytest.raises(UsageError):
+        eng.generate(ids, 4)  # 5 + 4 - 1 > 7
+    assert eng.generate(ids, 3).shape == (2, 3)
+    with pytest.raises(UsageError):
+        DecoderEngine(cfg, 2, 5, seed=1).prefill(ids)  # T + 1 > max_ctx
+
+
+def test_flag_cleared_by_prefill():
+    from paper_2206_01861_b200.decoder import DecoderEngine, GPTConfig
+
+    cfg = GPTConfig("tiny-flag", 1, 256, 4, 1024, 512, 8, 8, 16)
+    eng = DecoderEngine(cfg, 2, 16, seed=1, use_graph=False)
+    eng.flag.fill_(1)
+    eng.prefill(np.zeros((2, 4), np.int64))
+    eng.check_finite()

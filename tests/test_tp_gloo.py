@@ -60,7 +60,7 @@ class OracleOps:
     def igemm_s32(self, xq, w):
         return torch.from_numpy(O.igemm(xq, w.values))
 
-    def epilogue(self, acc, scales, w, bias):
+    def epilogue(self, acc, scales, w, bias, out=None):
         return O.dequant_epilogue(acc.numpy(), scales, w.rs, bias)
 
     def ln_quant(self, x, res, g, b):

@@ -49,3 +49,29 @@ def test_tp_cuda_ops_equal_fused_block(nccl_group, causal):
     sb = tp.shard_block(blk, ops, 0, 1)
     y = tp.tp_block_forward(x, sb, ops, causal, group=nccl_group, batch=2)
     assert torch.equal(y, ref)
+
+
+def test_forced_tp_decoder_graph_capture_matches_local(nccl_group):
+    """DecoderEngine(force_tp=True) on the 1-rank NCCL group routes o / 4hh
+    through tp.row_parallel_linear, so the MAX and int32 SUM all-reduces are
+    captured inside the decode step's CUDA graph; tokens and hidden states must
+    equal the local fused path bit for bit (graph replay of NCCL included)."""
+    import numpy as np
+
+    from paper_2206_01861_b200.decoder import DecoderEngine, GPTConfig
+
+    cfg = GPTConfig("tiny-tp", 2, 512, 8, 2048, 1024, 8, 8, 32)
+    ids = np.random.default_rng(3).integers(0, cfg.vocab, (4, 6))
+    res = []
+    for force in (False, True):
+        eng = DecoderEngine(cfg, 4, 16, seed=2, tp=(nccl_group, 0, 1) if force else None, force_tp=force,
+                            use_graph=True)
+        toks = [eng.prefill(ids).cpu().numpy()]
+        hs = [eng._buffers(4 * 6)["out"][:4].cpu().numpy()]
+        for _ in range(5):
+            toks.append(eng.step().cpu().numpy())
+            hs.append(eng._buffers(4)["out"][:4].cpu().numpy())
+        eng.check_finite()
+        res.append((np.stack(toks, 1), np.stack(hs)))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1].view(np.uint32), res[1][1].view(np.uint32))

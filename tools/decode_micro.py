@@ -36,7 +36,7 @@ def main():
     cx = torch.empty(B, d, device="cuda")
     lens = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
     pos = torch.full((B,), ctx - 1, dtype=torch.int32, device="cuda")
-    res["decode_attention"] = graph_time([lambda: N.call("zq_decode_attention_f32", qkv.data_ptr(), qkv.stride(0), kc.data_ptr(), vc.data_ptr(), 256, B, H, dh, lens.data_ptr(), 0.0625, cx.data_ptr(), cx.stride(0), N.stream_ptr())])
+    res["decode_attention"] = graph_time([lambda: N.call("zq_decode_attention_f32", qkv.data_ptr(), qkv.stride(0), kc.data_ptr(), vc.data_ptr(), 256, B, H, dh, lens.data_ptr(), 0.0625, cx.data_ptr(), cx.stride(0), 0, N.stream_ptr())])
     res["kv_append"] = graph_time([lambda: N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), B, 1, d, pos.data_ptr(), kc.data_ptr(), vc.data_ptr(), 256, N.stream_ptr())])
     for nm, (n, k) in {"qkv": (3 * d, d), "o": (d, d), "h4h": (f, d), "4hh": (d, f)}.items():
         sets = []
