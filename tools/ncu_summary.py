@@ -30,16 +30,21 @@ METRICS = [
 def report(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
+    to_mb = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
     res = []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")][:90]}
         for m, k, _ in METRICS:
             if m in hdr:
+                i = hdr.index(m)
                 try:
-                    d[k] = float(r[hdr.index(m)].replace(",", ""))
+                    v = float(r[i].replace(",", ""))
+                    if k.endswith("_MB"):
+                        v *= to_mb.get(units[i], 1.0)
+                    d[k] = v
                 except ValueError:
-                    d[k] = r[hdr.index(m)]
+                    d[k] = r[i]
         res.append(d)
     return res
 
