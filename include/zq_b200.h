@@ -62,6 +62,14 @@ int zq_quantize_tokenwise(const float* x, int64_t rows, int64_t cols, int64_t ld
 int zq_quantize_static(const float* x, int64_t rows, int64_t cols, int64_t ld_x, double scale,
                        int bits, int8_t* q, int64_t ld_q, int32_t* nonfinite_flag, void* stream);
 
+/* float64 inputs, as the reference reads them (no f32 round trip):
+ * compute_scale's max |x| per row (quant.py:80-95) and quantize_array's
+ * clamp(RHAFZ(x / scale)) with the f64 division (quant.py:98-113). */
+int zq_row_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ld_x, double* amax,
+                      int32_t* nonfinite_flag, void* stream);
+int zq_quantize_array_f64(const double* x, int64_t n, double scale, int bits, int8_t* q,
+                          int32_t* nonfinite_flag, void* stream);
+
 /* Replaces quant.quantize_weight_groupwise (pkg/src/lowbit/quant.py:236-255):
  * contiguous row groups (group_layout_for, quant.py:211-219), one f32 scale per
  * group, also writes the expanded per-row scale vector (QuantizedMatrix.row_scales).

@@ -40,6 +40,8 @@ _SIGS = {
     "zq_dequant_epilogue": [_p, _i64, _p, _f32, _p, _p, _i64, _i64, _p, _i64, _i32, _p],
     "zq_linear_full": [_p, _i64, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p],
     "zq_row_absmax": [_p, _i64, _i64, _i64, _p, _p, _p],
+    "zq_row_absmax_f64": [_p, _i64, _i64, _i64, _p, _p, _p],
+    "zq_quantize_array_f64": [_p, _i64, _f64, _i32, _p, _p, _p],
     "zq_quantize_with_absmax": [_p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p],
     "zq_gemm_set_trace": [_p],
     "zq_attention_debug": [_i32],

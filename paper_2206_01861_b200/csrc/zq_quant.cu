@@ -571,6 +571,68 @@ int zq_row_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x, floa
   return ZQ_OK;
 }
 
+// float64 inputs (quant.py:80-95 / :103-113 read their input as float64
+// without an f32 round trip): exact row max of |x| and RHAFZ(x / scale) with
+// the f64 division, +0.5 and floor of the reference (_round_half_away).
+__global__ void __launch_bounds__(256) row_absmax_f64_kernel(const double* __restrict__ x, int64_t cols,
+                                                             int64_t ld_x, double* __restrict__ amax,
+                                                             int32_t* __restrict__ flag) {
+  __shared__ double red[32];
+  const double* xr = x + (int64_t)blockIdx.x * ld_x;
+  double m = 0.0;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    const double a = xr[c];
+    bad |= !isfinite(a);
+    m = fmax(m, fabs(a));
+  }
+  if (bad && flag) atomicOr(flag, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) amax[blockIdx.x] = m;
+  }
+}
+
+__global__ void quantize_array_f64_kernel(const double* __restrict__ x, int64_t n, double scale, int qm,
+                                          int8_t* __restrict__ q, int32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = __ddiv_rn(x[i], scale);
+    bad |= !isfinite(x[i]);
+    const double a = fmin(floor(__dadd_rn(fabs(v), 0.5)), (double)qm);
+    const int k = (int)a;  // inf -> qm (np.clip); NaN raises on the host
+    q[i] = (int8_t)(v < 0.0 ? -k : k);
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+int zq_row_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ld_x, double* amax, int32_t* flag,
+                      void* stream) {
+  ZQ_CHECK_ARG(rows >= 1 && cols >= 1 && ld_x >= cols, ZQ_ERR_USAGE, "bad shape");
+  row_absmax_f64_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(x, cols, ld_x, amax, flag);
+  ZQ_LAUNCH_CHECK("row absmax (f64) launch");
+  return ZQ_OK;
+}
+
+int zq_quantize_array_f64(const double* x, int64_t n, double scale, int bits, int8_t* q, int32_t* flag,
+                          void* stream) {
+  ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d, expected one of (4, 8)", bits);
+  ZQ_CHECK_ARG(scale > 0.0, ZQ_ERR_USAGE, "quantization scale must be > 0, got %g", scale);
+  ZQ_CHECK_ARG(n >= 0, ZQ_ERR_USAGE, "bad size");
+  if (n == 0) return ZQ_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  quantize_array_f64_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, n, scale, qmax_of(bits), q, flag);
+  ZQ_LAUNCH_CHECK("quantize array (f64) launch");
+  return ZQ_OK;
+}
+
 int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x,
                             const float* amax, int bits, int8_t* q, int64_t ld_q,
                             float* token_scales, void* stream) {

@@ -90,21 +90,34 @@ def _device() -> torch.device:
 def as_device_f32(x) -> torch.Tensor:
     """Accept numpy / torch input; return a contiguous float32 CUDA tensor.
 
-    The reference pipeline is float32 throughout (tensor.py:24-29); float64
-    inputs are accepted only when they are exactly representable in float32
-    (otherwise the device kernels, which read f32, could round differently)."""
+    The reference coerces its inputs with `as_f32` (tensor.py:24-29: a numpy
+    float32 cast, round-to-nearest) before quantizing weights and activations
+    (quant.py:242, :261, :279); float64 input is cast the same way here."""
     if isinstance(x, torch.Tensor):
         t = x
     else:
-        a = np.asarray(x)
-        if a.dtype == np.float64 and a.size and np.all(np.isfinite(a)):
-            if not np.array_equal(a.astype(F32).astype(np.float64), a):
-                raise UsageError("float64 input is not exactly representable in float32")
-        t = torch.from_numpy(np.ascontiguousarray(a.astype(F32, copy=False)))
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x), dtype=F32))
     if t.device.type != "cuda":
         t = t.to(_device(), non_blocking=False)
     if t.dtype != torch.float32:
         t = t.float()
+    return t.contiguous()
+
+
+def _as_device_f64_or_f32(x) -> torch.Tensor:
+    """compute_scale / quantize_array read their input as float64 without an
+    f32 round trip (quant.py:90-93, :106-112): float32 input stays float32 (the
+    f64 widening is exact), anything else is widened to float64 on device."""
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        a = np.asarray(x)
+        t = torch.from_numpy(np.ascontiguousarray(a if a.dtype in (np.float32, np.float64) else
+                                                  a.astype(np.float64)))
+    if t.device.type != "cuda":
+        t = t.to(_device(), non_blocking=False)
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
     return t.contiguous()
 
 
@@ -143,15 +156,21 @@ class FiniteFlag:
 
 
 def compute_scale(values, bits: int) -> float:
-    """quant.py:80-95: f32(max|x| / qmax); 1.0 for an all-zero slice."""
+    """quant.py:80-95: f32(max|x| / qmax); 1.0 for an all-zero slice.  The max
+    runs on device over the input's own precision (float64 stays float64)."""
     _check_bits(bits)
-    v = as_device_f32(values).reshape(1, -1)
+    v = _as_device_f64_or_f32(values).reshape(1, -1)
     if v.numel() == 0:
         raise UsageError("compute_scale called on an empty slice")
-    amax = torch.empty(1, dtype=torch.float32, device=v.device)
     flag = FiniteFlag()
-    N.call("zq_row_absmax", v.data_ptr(), 1, v.shape[1], v.shape[1], amax.data_ptr(), flag.ptr,
-           N.stream_ptr())
+    if v.dtype == torch.float64:
+        amax = torch.empty(1, dtype=torch.float64, device=v.device)
+        N.call("zq_row_absmax_f64", v.data_ptr(), 1, v.shape[1], v.shape[1], amax.data_ptr(), flag.ptr,
+               N.stream_ptr())
+    else:
+        amax = torch.empty(1, dtype=torch.float32, device=v.device)
+        N.call("zq_row_absmax", v.data_ptr(), 1, v.shape[1], v.shape[1], amax.data_ptr(), flag.ptr,
+               N.stream_ptr())
     if int(flag.t.item()) != 0:
         raise ValueError("compute_scale called on non-finite values")
     m = float(amax.item())
@@ -165,13 +184,19 @@ def quantize_array(x, scale: float, bits: int) -> torch.Tensor:
     _check_bits(bits)
     if not scale > 0:
         raise UsageError(f"quantization scale must be > 0, got {scale}")
-    xt = as_device_f32(x)
+    xt = _as_device_f64_or_f32(x)
     shape = xt.shape
+    flag = FiniteFlag()
+    if xt.dtype == torch.float64:
+        out = torch.empty(shape, dtype=torch.int8, device=xt.device)
+        N.call("zq_quantize_array_f64", xt.data_ptr(), xt.numel(), float(scale), bits, out.data_ptr(), flag.ptr,
+               N.stream_ptr())
+        flag.check("values")
+        return out
     x2 = xt.reshape(1, -1) if xt.dim() != 2 else xt
     rows, cols = x2.shape
     out = padded_int8(rows, cols)
     if x2.numel():
-        flag = FiniteFlag()
         N.call("zq_quantize_static", x2.data_ptr(), rows, cols, cols, float(scale), bits,
                out.data_ptr(), out.stride(0), flag.ptr, N.stream_ptr())
         flag.check("values")
@@ -179,7 +204,7 @@ def quantize_array(x, scale: float, bits: int) -> torch.Tensor:
 
 
 def quantize_value(x: float, scale: float, bits: int) -> int:
-    """quant.py:116-118"""
+    """quant.py:116-118 (a Python float is a float64, as in the reference)."""
     return int(quantize_array(np.asarray([x]), scale, bits)[0].item())
 
 

@@ -305,3 +305,33 @@ def test_gelu_estimate_within_its_bracket(zq):
     assert np.all(rel <= b[nz]), (rel.max(), x[nz][np.argmax(rel - b[nz])])
     assert rel.max() <= 2.0 ** -17, rel.max()  # the bracket gelu_quant_kernel assumes
     assert np.all(e[~nz] == 0.0)
+
+
+def test_float64_inputs_follow_the_reference(zq):
+    """compute_scale / quantize_array / quantize_value read float64 input in
+    float64 (quant.py:80-118); the other quantizers cast to float32 first
+    (as_f32, quant.py:242, :261, :279) instead of rejecting it."""
+    from paper_2206_01861_b200 import quant
+
+    assert quant.quantize_value(0.1, 0.01, 8) == 10           # 0.1 / 0.01 in f64 = 10.000000000000002
+    assert quant.quantize_value(1.0, 2.0 / 127.0, 8) == 64    # exact f64 tie 63.5 -> away from zero
+    assert quant.quantize_value(-1.0, 2.0 / 127.0, 8) == -64
+    x = np.array([0.1, -0.25000000000000006, 1e-300, 3.0, -1e300, 0.0])
+    ref = O.quantize_array(x, 0.05, 8)
+    assert np.array_equal(h(quant.quantize_array(x, 0.05, 8)), ref)
+    v = np.array([0.30000000000000004, -0.1, 1e-320])
+    assert quant.compute_scale(v, 8) == O.compute_scale(v, 8) == float(np.float32(0.30000000000000004 / 127))
+    assert quant.compute_scale(np.array([1, -254, 3]), 8) == 2.0       # integer input -> exact f64
+    rng = np.random.default_rng(0)
+    w64 = rng.standard_normal((64, 48)) * 0.02
+    qm = quant.quantize_weight_groupwise(w64, 4, 8)
+    vals, gs, _ = O.quantize_weight_groupwise(w64.astype(np.float32), 4, 8)
+    assert np.array_equal(h(qm.values), vals) and np.array_equal(h(qm.group_scales), gs)
+    x64 = rng.standard_normal((7, 33))
+    qa = quant.quantize_activation_tokenwise(x64, 8)
+    q_ref, s_ref = O.quantize_activation_tokenwise(x64.astype(np.float32), 8)
+    assert np.array_equal(h(qa.values), q_ref) and np.array_equal(h(qa.token_scales), s_ref)
+    with pytest.raises(ValueError):
+        quant.quantize_array(np.array([1.0, np.inf]), 0.1, 8)
+    with pytest.raises(ValueError):
+        quant.compute_scale(np.array([np.nan]), 8)
