@@ -243,6 +243,30 @@ int zq_attention_debug(int mode);
  * 1 operands landed, 2 split done, 3 S done, 4 P in TMEM, 5 O done, 6 stored). */
 int zq_attention_set_trace(unsigned long long* buf);
 
+
+/* ---- Order-exact float32 forward for static calibration (zq_calib.cu) ----
+ * The reference calibrates on its FLOAT model (evaluate.py:168-196 over
+ * transformer.py:405-440); these restate its numpy arithmetic so the
+ * calibrated scales come out bit-identical. */
+
+/* tensor.matmul(a, w.T) (+ bias) (tensor.py:37-56, transformer.py:405-410):
+ * p-ascending f32 sum of separately rounded products from +0.0. */
+int zq_matmul_f32_seq(const float* a, int64_t lda, const float* w, int64_t ldw, const float* bias, int64_t M,
+                      int64_t N, int64_t K, float* out, int64_t ldo, void* stream);
+
+/* transformer.attention (transformer.py:413-440) over one sequence of t tokens:
+ * q, k, v = columns [0, d), [d, 2d), [2d, 3d) of qkv; numpy's f32 exp and
+ * pairwise row sum inside tensor.softmax (tensor.py:94-99).  scratch: heads*t*t
+ * floats. */
+int zq_attention_exact_f32(const float* qkv, int64_t ld_qkv, int t, int heads, int head_dim, int causal,
+                           float inv_scale, float* scratch, float* ctx, int64_t ld_ctx, void* stream);
+
+/* out2 = [max, min] of x[0..n) (Calibrator.observe, quant.py:305-317). */
+int zq_minmax_f32(const float* x, int64_t n, float* out2, int32_t* nonfinite_flag, void* stream);
+
+/* y = numpy's float32 exp(x) (diagnostics / parity of the calibration forward). */
+int zq_np_expf(const float* x, int64_t n, float* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -574,3 +574,79 @@ def cephes_erf(x: float) -> float:
     else:
         p, q = _polevl(x, _ERF_R, 5), _p1evl(x, _ERF_S, 6)
     return 1.0 - (e * p) / q
+
+
+# ---------------------------------------------------------------------------
+# Static calibration on the float model (evaluate.py:168-196)
+# ---------------------------------------------------------------------------
+
+
+def numpy_expf(x) -> np.ndarray:
+    """numpy 2.x's float32 exp (simd_exp_f32, the kernel behind np.exp on
+    float32 arrays in tensor.softmax, tensor.py:94-99), restated: Cody-Waite
+    range reduction with FMA, a [5/2] rational minimax, scaling by 2^k.  FMA is
+    emulated in float64 (a*b is exact there); pinned against np.exp in
+    tests/test_oracle_golden.py.  The GPU restates it as np_expf
+    (csrc/zq_calib.cu)."""
+    x = np.asarray(x, dtype=F32)
+    d = np.float64
+
+    def fma(a, b, c):  # f32(a*b + c), one rounding (a*b exact in f64)
+        return (np.asarray(a, d) * np.asarray(b, d) + np.asarray(c, d)).astype(F32)
+
+    P = [F32(c) for c in (9.999999999980870924916e-01, 7.257664613233124478488e-01, 2.473615434895520810817e-01,
+                          5.114512081637298353406e-02, 6.757896990527504603057e-03, 5.082762527590693718096e-04)]
+    Q1, Q2 = F32(-2.742335390411667452936e-01), F32(2.159509375685829852307e-02)
+    with np.errstate(all="ignore"):
+        quad = (x * F32(1.442695040888963407359924681001892137)).astype(F32)
+        quad = ((quad + F32(12582912.0)).astype(F32) - F32(12582912.0)).astype(F32)
+        r = fma(quad, F32(-6.93145752e-1), x)
+        r = fma(quad, F32(-1.42860677e-6), r)
+        num = fma(P[5], r, P[4])
+        for c in (P[3], P[2], P[1], P[0]):
+            num = fma(num, r, c)
+        den = fma(fma(Q2, r, Q1), r, F32(1.0))
+        v = (num / den).astype(F32)
+        out = (v.astype(d) * np.exp2(quad.astype(d))).astype(F32)
+    out = np.where(x >= F32(88.72283935546875), F32(np.inf), out)
+    out = np.where(x <= F32(-103.97208404541015625), F32(0.0), out)
+    return np.where(np.isnan(x), x, out).astype(F32)
+
+
+def float_block_forward(x, w: dict, num_heads: int, causal: bool, layer: int = 0, tap=None) -> np.ndarray:
+    """pkg/src/lowbit/transformer.py:443-486 for float weights (FullAct
+    everywhere, _linear = tensor.matmul + bias, transformer.py:405-410)."""
+    x = np.ascontiguousarray(x, dtype=F32)
+
+    def lin(inp, a, b):
+        out = matmul_f32(inp, np.ascontiguousarray(w[a].T))
+        out += np.asarray(w[b], F32)[None, :]
+        return out
+
+    if tap is not None:
+        tap("attn_in", layer, x)
+    ctx = attention(lin(x, "w_q", "b_q"), lin(x, "w_k", "b_k"), lin(x, "w_v", "b_v"), num_heads, causal)
+    if tap is not None:
+        tap("attn_proj_in", layer, ctx)
+    h = layer_norm_numpy(x + lin(ctx, "w_o", "b_o"), w["ln1_gamma"], w["ln1_beta"])
+    if tap is not None:
+        tap("ffc_in", layer, h)
+    z = gelu(lin(h, "w_h4h", "b_h4h"))
+    if tap is not None:
+        tap("ffc_mid", layer, z)
+    return layer_norm_numpy(h + lin(z, "w_4hh", "b_4hh"), w["ln2_gamma"], w["ln2_beta"])
+
+
+def calibrate_model(embedding, blocks: list, num_heads: int, causal: bool, batches, momentum: float = 0.95,
+                    bits: int = 8) -> dict:
+    """pkg/src/lowbit/evaluate.py:168-196: {key: (x_max, x_min, scale)}."""
+    cals: dict = {}
+
+    def tap(site, layer, x):
+        cals.setdefault(f"layer{layer}.{site}", Calibrator(momentum)).observe(x)
+
+    for ids in batches:
+        x = np.asarray(embedding, F32)[np.asarray(ids, np.int64)]
+        for li, w in enumerate(blocks):
+            x = float_block_forward(x, w, num_heads, causal, li, tap)
+    return {k: (c.x_max, c.x_min, c.finalize(bits)) for k, c in sorted(cals.items())}

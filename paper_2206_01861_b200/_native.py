@@ -54,6 +54,10 @@ _SIGS = {
     "zq_linear_kv": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i32, _i64,
                      _p],
     "zq_l2_persist": [_p, _p, _i64, _p],
+    "zq_matmul_f32_seq": [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p],
+    "zq_attention_exact_f32": [_p, _i64, _i32, _i32, _i32, _i32, _f32, _p, _p, _i64, _p],
+    "zq_minmax_f32": [_p, _i64, _p, _p, _p],
+    "zq_np_expf": [_p, _i64, _p, _p],
     "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
 }
 

@@ -782,6 +782,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_init(done_bar, 1);
     fence_barrier_init();
   }
+  __syncwarp();  // reconverge warp 0 after the lane-0 setup before the CTA barrier
   if (warp == 1) tmem_alloc(tmem_slot, MP < 32 ? 32 : MP);
   tc_fence_before();
   __syncthreads();

@@ -421,12 +421,23 @@ class Calibrator:
             raise UsageError(f"momentum must be in (0, 1), got {self.momentum}")
 
     def observe(self, x) -> None:
-        xt = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
-        xt = xt.to(_device())
-        if not bool(torch.isfinite(xt).all()):
-            raise ValueError("calibrator observed non-finite values")
-        bmax = float(xt.max())
-        bmin = float(xt.min())
+        """quant.py:305-317: batch max / min reduced on device (zq_minmax_f32)."""
+        xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        xt = xt.to(_device()).contiguous()
+        if xt.dtype != torch.float32:  # the reference reduces the input's own dtype
+            xt = xt.double()
+            if not bool(torch.isfinite(xt).all()):
+                raise ValueError("calibrator observed non-finite values")
+            hm = torch.stack([xt.max(), xt.min()]).cpu()
+        else:
+            mm = torch.empty(2, dtype=torch.float32, device=xt.device)
+            flag = FiniteFlag()
+            N.call("zq_minmax_f32", xt.data_ptr(), xt.numel(), mm.data_ptr(), flag.ptr, N.stream_ptr())
+            hm = mm.cpu()
+            if int(flag.t.item()) != 0:
+                raise ValueError("calibrator observed non-finite values")
+        bmax = float(hm[0])
+        bmin = float(hm[1])
         if self.observed_batches == 0:
             self.x_max, self.x_min = bmax, bmin
         else:

@@ -333,43 +333,67 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
     return y
 
 
+def _matmul_seq(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None) -> torch.Tensor:
+    """tensor.matmul(x, w.T) (+= bias), transformer.py:405-410, order-exact."""
+    m, k = x.shape
+    n = w.shape[0]
+    out = torch.empty((m, n), dtype=torch.float32, device=x.device)
+    N.call("zq_matmul_f32_seq", x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), N.ptr(bias), m, n, k,
+           out.data_ptr(), out.stride(0), N.stream_ptr())
+    return out
+
+
 def float_block_forward(x: torch.Tensor, w: dict, num_heads: int, causal: bool, layer: int = 0,
                         tap=None) -> torch.Tensor:
     """transformer.py:443-486 with float weights (PrecisionConfig.full()): the
-    calibration forward.  `w` holds float32 device tensors (w_q .. ln2_beta);
-    `tap(site, layer, x)` sees the float tensor entering each weight GEMM."""
-    def lin(inp, wn, bn):
-        return torch.addmm(w[bn], inp, w[wn].t())
-
-    if tap is not None:
-        tap("attn_in", layer, x)
-    q, k, v = lin(x, "w_q", "b_q"), lin(x, "w_k", "b_k"), lin(x, "w_v", "b_v")
+    calibration forward, bit-identical to the reference's numpy arithmetic
+    (csrc/zq_calib.cu: sequential f32 matmuls, the exact float attention with
+    numpy's exp and pairwise softmax sum; the exact LN / GeLU kernels' f32
+    outputs).  `x` is one sequence [t, d]; `w` holds float32 device tensors
+    (w_q .. ln2_beta); `tap(site, layer, x)` sees the float tensor entering
+    each weight GEMM."""
     t, d = x.shape
     dh = d // num_heads
-    heads = lambda z: z.reshape(1, t, num_heads, dh).transpose(1, 2)  # noqa: E731
-    ctx = torch.nn.functional.scaled_dot_product_attention(
-        heads(q), heads(k), heads(v), is_causal=causal,
-        scale=float(np.float32(1.0 / math.sqrt(dh)))).transpose(1, 2).reshape(t, d)
+    if tap is not None:
+        tap("attn_in", layer, x)
+    qkv = torch.empty((t, 3 * d), dtype=torch.float32, device=x.device)
+    for i, (wn, bn) in enumerate((("w_q", "b_q"), ("w_k", "b_k"), ("w_v", "b_v"))):
+        qkv[:, i * d:(i + 1) * d] = _matmul_seq(x, w[wn], w[bn])
+    ctx = torch.empty((t, d), dtype=torch.float32, device=x.device)
+    scratch = torch.empty(num_heads * t * t, dtype=torch.float32, device=x.device)
+    N.call("zq_attention_exact_f32", qkv.data_ptr(), qkv.stride(0), t, num_heads, dh, int(causal),
+           float(np.float32(1.0 / math.sqrt(dh))), scratch.data_ptr(), ctx.data_ptr(), ctx.stride(0),
+           N.stream_ptr())
     if tap is not None:
         tap("attn_proj_in", layer, ctx)
-    h = torch.nn.functional.layer_norm(x + lin(ctx, "w_o", "b_o"), (d,), w["ln1_gamma"], w["ln1_beta"], LN_EPS)
+    attn_out = _matmul_seq(ctx, w["w_o"], w["b_o"])
+    h = torch.empty_like(x)
+    igemm.layer_norm_quantize(x, w["ln1_gamma"], w["ln1_beta"], 8, LN_EPS, residual=attn_out, ln_out=h,
+                              check_finite=False)
     if tap is not None:
         tap("ffc_in", layer, h)
-    z = torch.nn.functional.gelu(lin(h, "w_h4h", "b_h4h"))
+    u = _matmul_seq(h, w["w_h4h"], w["b_h4h"])
+    z = torch.empty_like(u)
+    igemm.gelu_quantize(u, 8, gelu_out=z, check_finite=False)
     if tap is not None:
         tap("ffc_mid", layer, z)
-    f = lin(z, "w_4hh", "b_4hh")
-    return torch.nn.functional.layer_norm(h + f, (d,), w["ln2_gamma"], w["ln2_beta"], LN_EPS)
+    f = _matmul_seq(z, w["w_4hh"], w["b_4hh"])
+    y = torch.empty_like(x)
+    igemm.layer_norm_quantize(h, w["ln2_gamma"], w["ln2_beta"], 8, LN_EPS, residual=f, ln_out=y,
+                              check_finite=False)
+    return y
 
 
-def calibrate_static_scales(float_blocks: list[dict], batches, num_heads: int, causal: bool,
-                            momentum: float = 0.95, bits: int = 8) -> dict[str, float]:
-    """evaluate.calibrate_model (evaluate.py:168-200) on device: every calibration
-    batch (float32 [tokens, d] block-0 inputs) runs through the float blocks with
-    one `quant.Calibrator` per GEMM-input site "layer{L}.{site}" (momentum
-    min/max, quant.py:289-330, extrema reduced on device); returns the finalized
-    static scales for `block_forward(..., static_scales=...)` under a
-    `PrecisionConfig(..., activation_static=True)`."""
+@dataclass
+class SiteCalibration:
+    """evaluate.py:159-163"""
+
+    x_max: float
+    x_min: float
+    scale: float
+
+
+def _calibrators(momentum: float):
     cals: dict[str, quant.Calibrator] = {}
 
     def tap(site, layer, x):
@@ -378,6 +402,48 @@ def calibrate_static_scales(float_blocks: list[dict], batches, num_heads: int, c
             cals[key] = quant.Calibrator(momentum=momentum)
         cals[key].observe(x)
 
+    return cals, tap
+
+
+def calibrate_model(embedding, float_blocks: list[dict], num_heads: int, causal: bool, batches,
+                    momentum: float = 0.95, bits: int = 8) -> dict[str, SiteCalibration]:
+    """evaluate.calibrate_model (evaluate.py:168-196) on device: every batch (a
+    1-d token-id sequence, consumed in order) runs embed -> the float blocks
+    (model_forward with PrecisionConfig.full(), transformer.py:489-532) with one
+    momentum Calibrator per GEMM-input site "layer{L}.{site}" (quant.py:289-330).
+    The float forward is order-exact, so x_max / x_min / scale are
+    bit-identical to the reference's."""
+    cals, tap = _calibrators(momentum)
+    emb = as_device_f32(embedding)
+    dev_blocks = [{k: as_device_f32(v) for k, v in b.items() if k != "num_heads"} for b in float_blocks]
+    n = 0
+    for ids in batches:
+        ids_t = torch.as_tensor(np.asarray(ids, dtype=np.int64)).reshape(-1)
+        if ids_t.numel() == 0:
+            raise UsageError("empty token sequence")
+        if int(ids_t.min()) < 0 or int(ids_t.max()) >= emb.shape[0]:
+            raise UsageError(f"token id out of range [0, {emb.shape[0]})")
+        x = emb.index_select(0, ids_t.to(emb.device))
+        for li, w in enumerate(dev_blocks):
+            x = float_block_forward(x, w, num_heads, causal, li, tap)
+        n += 1
+    if n == 0:
+        raise UsageError("calibration needs at least one batch")
+    return {k: SiteCalibration(c.x_max, c.x_min, c.finalize(bits)) for k, c in sorted(cals.items())}
+
+
+def static_scales_from(calibration: dict[str, SiteCalibration]) -> dict[str, float]:
+    """evaluate.py:199-200"""
+    return {k: sc.scale for k, sc in calibration.items()}
+
+
+def calibrate_static_scales(float_blocks: list[dict], batches, num_heads: int, causal: bool,
+                            momentum: float = 0.95, bits: int = 8) -> dict[str, float]:
+    """Calibration from block-0 inputs: every batch (float32 [tokens, d], one
+    sequence) runs through the float blocks (the order-exact forward above)
+    with one Calibrator per site; returns the finalized static scales for
+    `block_forward(..., static_scales=...)` under activation_static=True."""
+    cals, tap = _calibrators(momentum)
     dev_blocks = [{k: as_device_f32(v) for k, v in b.items() if k != "num_heads"} for b in float_blocks]
     n = 0
     for xb in batches:

@@ -171,3 +171,31 @@ def test_cephes_erf_is_scipy_erf():
     ref = erf(xs)
     mine = np.asarray([O.cephes_erf(float(v)) for v in xs])
     assert np.array_equal(mine, ref)
+
+
+def test_numpy_expf_restatement_is_np_exp():
+    """Pins the float32 exp the calibration forward restates (numpy's SIMD
+    simd_exp_f32; csrc/zq_calib.cu np_expf): identical to np.exp on float32,
+    although 39% of np.exp's results are not the correctly rounded exp."""
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([-rng.random(400000) * 30, rng.uniform(-104, -80, 100000), rng.uniform(-5, 5, 100000),
+                         [-np.inf, -200.0, -103.97208404541015625, -87.3, -0.0, 0.0, 88.72283935546875, 50.0]])
+    xs = xs.astype(F32)
+    with np.errstate(all="ignore"):
+        ref = np.exp(xs)
+    assert np.array_equal(O.numpy_expf(xs), ref)
+    assert (O.numpy_expf(xs[:1000]) != np.exp(xs[:1000].astype(np.float64)).astype(F32)).any()
+
+
+def test_oracle_calibration_matches_reference_golden():
+    """oracle.calibrate_model (evaluate.py:168-196 restated) reproduces the
+    reference's own calibration of the fixture model bit for bit."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "calibration.npz"))
+    blocks = [{n[3:]: g[n] for n in g.files if n.startswith(f"l{li}_")} for li in range(int(g["layers"]))]
+    batches = [g[f"batch{i}"] for i in range(3)]
+    cal = O.calibrate_model(g["embedding"], blocks, int(g["num_heads"]), True, batches)
+    assert list(cal) == list(g["site_keys"])
+    for k, xm, xn, sc in zip(g["site_keys"], g["site_xmax"], g["site_xmin"], g["site_scale"]):
+        assert cal[k] == (xm, xn, sc), (k, cal[k], (xm, xn, sc))
