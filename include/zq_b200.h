@@ -148,6 +148,22 @@ int zq_linear_full(const float* x, int64_t ld_x, const void* wq, int64_t ld_w, i
                    const float* w_row_scales, const float* bias, int64_t M, int64_t N,
                    int64_t K, float* out, int64_t ld_out, void* stream);
 
+/* Weight-only tensor-core path (tolerance mode of igemm.quantized_linear(FullAct),
+ * pkg/src/lowbit/igemm.py:127-130; the paper's W8A16 / A8/16 deployment).
+ * Step 1 splits each activation row, scaled by a power of two 2^e that puts its
+ * max in [2^14, 2^15), into terms = 1 (fp16, "A16") or 2 (fp16 hi + lo, ~22
+ * significant bits) 16-bit arrays [M, ld_h] and writes row_inv[i] = 2^-e. */
+int zq_act_split16(const float* x, int64_t ld_x, int64_t M, int64_t K, int terms, void* hi, void* lo,
+                   int64_t ld_h, float* row_inv, int32_t* nonfinite_flag, void* stream);
+
+/* Step 2: out = ((acc * row_inv[i]) * s_w[j]) + bias[j], acc = sum_k (hi [+ lo])[i,k] * q[j,k]
+ * on tcgen05 kind::f16 CTA pairs (f32 accumulators), the int8 / packed INT4 weight
+ * rows converted to f16 in shared memory (exact).  a_lo = NULL for one term.
+ * ld_a % 8 == 0, ld_w % 32 == 0 (weight rows as zq_linear).  out_type ZQ_OUT_*. */
+int zq_linear_wo(const void* a_hi, const void* a_lo, int64_t ld_a, const float* row_inv, const void* wq,
+                 int64_t ld_w, int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N,
+                 int64_t K, void* out, int64_t ld_out, int out_type, void* stream);
+
 /* Row absmax (f32 bit patterns, non-negative) for the tensor-parallel token-scale
  * all-reduce: amax[i] = max_j |x[i, j]|. */
 int zq_row_absmax(const float* x, int64_t rows, int64_t cols, int64_t ld_x, float* amax,

@@ -154,19 +154,47 @@ def fused_linear(xq: QuantizedActivation, w: QuantizedMatrix, bias=None,
     return out
 
 
-def full_linear(x, w: QuantizedMatrix, bias=None) -> torch.Tensor:
-    """FullAct: x @ dequant(w).T + bias with the reference's sequential float32
-    accumulation (igemm.py:127-130, tensor.py:37-56); bit-exact."""
+FULL_PRECISIONS = ("exact", "f16", "f16x2")
+
+
+def full_linear(x, w: QuantizedMatrix, bias=None, precision: str = "exact",
+                out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """FullAct: x @ dequant(w).T + bias (igemm.py:127-130).
+
+    precision="exact": the reference's sequential float32 accumulation
+    (tensor.py:37-56), bit-exact, CUDA cores.  "f16" / "f16x2" (B200 tolerance
+    modes, the paper's A16 deployment): tcgen05 kind::f16 CTA pairs with the
+    weights converted int8/INT4 -> f16 in shared memory and each activation row
+    scaled by a power of two into 1 (fp16) or 2 (hi + lo, ~22 bits) f16 terms.
+    Tolerances vs the reference (tests/test_wo_gpu.py): f16 max|err| <= 2e-3 *
+    max|ref|, f16x2 <= 5e-5 * max|ref|."""
+    if precision not in FULL_PRECISIONS:
+        raise UsageError(f"full_linear precision must be one of {FULL_PRECISIONS}, got {precision!r}")
     xt = as_device_f32(x)
     if xt.dim() != 2 or xt.shape[1] != w.cols:
         raise ShapeError(f"matmul inner dimensions differ: {tuple(xt.shape)} x {(w.cols, w.rows)}")
     m, k = xt.shape
     n = w.rows
     b = None if bias is None else as_device_f32(bias).reshape(-1)
-    out = torch.empty((m, n), dtype=torch.float32, device=xt.device)
     wp, ld_w, wb = w.weight_operand()
-    N.call("zq_linear_full", xt.data_ptr(), xt.stride(0), wp, ld_w, wb, w.row_scales().data_ptr(),
-           N.ptr(b), m, n, k, out.data_ptr(), out.stride(0), N.stream_ptr())
+    if precision == "exact":
+        if out_dtype != torch.float32:
+            raise UsageError("the exact FullAct path produces float32 (as the reference)")
+        out = torch.empty((m, n), dtype=torch.float32, device=xt.device)
+        N.call("zq_linear_full", xt.data_ptr(), xt.stride(0), wp, ld_w, wb, w.row_scales().data_ptr(),
+               N.ptr(b), m, n, k, out.data_ptr(), out.stride(0), N.stream_ptr())
+        return out
+    terms = 1 if precision == "f16" else 2
+    ld_h = (k + 7) // 8 * 8
+    hi = torch.empty((m, ld_h), dtype=torch.float16, device=xt.device)
+    lo = torch.empty((m, ld_h), dtype=torch.float16, device=xt.device) if terms == 2 else None
+    row_inv = torch.empty(m, dtype=torch.float32, device=xt.device)
+    N.call("zq_act_split16", xt.data_ptr(), xt.stride(0), m, k, terms, hi.data_ptr(), N.ptr(lo), ld_h,
+           row_inv.data_ptr(), None, N.stream_ptr())
+    out = torch.empty((m, n), dtype=out_dtype, device=xt.device)
+    N.call("zq_linear_wo", hi.data_ptr(), N.ptr(lo), ld_h, row_inv.data_ptr(), wp, ld_w, wb,
+           w.row_scales().data_ptr(), N.ptr(b), m, n, k, out.data_ptr(), out.stride(0), _OUT_CODES[out.dtype],
+           N.stream_ptr())
     return out
 
 
