@@ -1,7 +1,7 @@
 """Benchmark driver (contract in the task statement; workload = BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload all|bert|c1|gemm-large|gpt3-350m|gptj-6b|neox-20b]
+                    [--workload all|bert|c1|c1-f16|gemm-large|wo-gemm|gpt3-350m|gptj-6b|neox-20b]
 
 Headline workload (the JSON line's metric/value): BERT-base full INT8 W8A8
 encoder forward, batch 32 x seq 128, random-init weights (Gaussian 0.02),
@@ -865,7 +865,85 @@ def gemm_large_measure(steps: int, warmup: int, rank: int, world: int):
                          "peak_basis": INT8_PEAK_BASIS.format(basis=basis, **peaks)}}
 
 
-SECONDARY = ("c1", "c1-f16", "gemm-large", "gpt3-350m", "gptj-6b", "neox-20b")
+WO_SHAPES = [("NeoX-20B QKV prefill", 2048, 18432, 6144), ("NeoX-20B h4h prefill", 2048, 24576, 6144),
+             ("NeoX-20B 4hh prefill", 2048, 6144, 24576)]
+
+
+def wo_gemm_measure(steps: int, warmup: int, rank: int, world: int):
+    """The tensor-core FullAct (weight-only, W8A16 / the A16 sites of W8A8/16)
+    linear at NeoX-20B prefill shapes (batch 16 x 128 tokens): activation split
+    (f32 -> power-of-two-scaled f16 terms) + the converted-weight CTA-pair GEMM
+    (int8 weights -> f16 in smem, tcgen05 kind::f16), f16 out.  TFLOP/s against
+    the measured bf16 dense peak; `steps` launches per shape in one CUDA graph."""
+    import torch
+
+    from paper_2206_01861_b200 import _native as N
+    from paper_2206_01861_b200 import quant
+
+    peaks, basis = load_peaks()
+    pbf = peaks["bf16_tflops"] * 1e12
+    res = []
+    gen = torch.Generator(device="cuda").manual_seed(11 + rank)
+    for label, m, n, k in WO_SHAPES:
+        for wbits, terms in ((8, 1), (8, 2), (4, 1)):
+            w = torch.randn(n, k, generator=gen, device="cuda") * 0.02
+            wq = quant.quantize_weight_groupwise(w, 128, wbits)
+            del w
+            xs = [torch.randn(m, k, generator=gen, device="cuda") for _ in range(2)]
+            ld_h = (k + 7) // 8 * 8
+            hi = torch.empty(m, ld_h, dtype=torch.float16, device="cuda")
+            lo = torch.empty(m, ld_h, dtype=torch.float16, device="cuda") if terms == 2 else None
+            ri = torch.empty(m, device="cuda")
+            out = torch.empty(m, n, dtype=torch.float16, device="cuda")
+            wp, ld_w, wb = wq.weight_operand()
+            rs = wq.row_scales()
+
+            def launch(i):
+                x = xs[i % 2]
+                N.call("zq_act_split16", x.data_ptr(), x.stride(0), m, k, terms, hi.data_ptr(), N.ptr(lo), ld_h,
+                       ri.data_ptr(), None, N.stream_ptr())
+                N.call("zq_linear_wo", hi.data_ptr(), N.ptr(lo), ld_h, ri.data_ptr(), wp, ld_w, wb, rs.data_ptr(),
+                       None, m, n, k, out.data_ptr(), out.stride(0), N.OUT_F16, N.stream_ptr())
+
+            for i in range(warmup):
+                launch(i)
+            torch.cuda.synchronize()
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                for i in range(steps):
+                    launch(i)
+            g_.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(torch.cuda.current_device()) as clk:
+                a.record()
+                g_.replay()
+                b.record()
+                torch.cuda.synchronize()
+            sec = a.elapsed_time(b) * 1e-3 / steps
+            fl = 2.0 * m * n * k
+            res.append({"shape": label, "M": m, "N": n, "K": k, "w_bits": wbits,
+                        "mode": "f16" if terms == 1 else "f16x2", "us": 1e6 * sec, "tflops": fl / sec / 1e12,
+                        "frac_of_bf16_peak": fl / sec / pbf, "clocks": clk.summary()})
+            del xs, hi, lo, out, wq
+            torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    w8 = [r for r in res if r["w_bits"] == 8 and r["mode"] == "f16"]
+    best = max(w8, key=lambda r: r["tflops"])
+    return {"metric": "W8A16 weight-only linear TFLOP/s at NeoX-20B prefill shapes (vs bf16 peak)",
+            "value": world * best["tflops"], "unit": "TFLOP/s", "n_gpus": world, "steps": steps, "warmup": warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic", "config": {"workload": "FullAct tensor-core mode: act split + converted-weight "
+                                                        "pair GEMM, f16 out; value = best W8 f16 shape, per shape below",
+                                            "l2": "2 rotating activation inputs; weights 113-302 MB (> L2)"},
+            "shapes": res,
+            "roofline": {"bound": "tensor", "achieved": best["tflops"], "peak": pbf / 1e12, "unit": "TFLOP/s",
+                         "frac": best["frac_of_bf16_peak"], "traffic": None,
+                         "peak_basis": f"measured bf16 dense ({basis})"}}
+
+
+SECONDARY = ("c1", "c1-f16", "gemm-large", "wo-gemm", "gpt3-350m", "gptj-6b", "neox-20b")
 
 
 def secondary_workloads(rank: int, world: int, dist):
@@ -884,6 +962,8 @@ def secondary_workloads(rank: int, world: int, dist):
                 r = c1_measure(20, 5, rank, world, out_dtype=torch.float16)
             elif name == "gemm-large":
                 r = gemm_large_measure(10, 3, rank, world)
+            elif name == "wo-gemm":
+                r = wo_gemm_measure(10, 3, rank, world)
             else:
                 r = gpt_measure(name, 2, 3, rank, world, dist, cpu=False)
         except Exception as e:  # noqa: BLE001 - recorded, the headline stands
@@ -905,6 +985,8 @@ def run_single(args, rank: int, world: int, dist):
                           out_dtype=torch.float16 if args.workload == "c1-f16" else None)
     elif args.workload == "gemm-large":
         line = gemm_large_measure(args.steps, args.warmup, rank, world)
+    elif args.workload == "wo-gemm":
+        line = wo_gemm_measure(args.steps, args.warmup, rank, world)
     else:
         line = gpt_measure(args.workload, args.steps, args.warmup, rank, world, dist)
     if line is not None:

@@ -289,17 +289,21 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int,
     return ctx
 
 
-def _linear_site(x, w: QuantizedMatrix, bias, am):
+def _linear_site(x, w: QuantizedMatrix, bias, am, full_act: str = "exact"):
     if isinstance(am, FullAct):
-        return igemm.full_linear(x, w, bias)
+        return igemm.full_linear(x, w, bias, precision=full_act)
     return igemm.quantized_linear(x, w, bias, am)
 
 
 def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: bool, layer: int = 0,
-                  static_scales: dict[str, float] | None = None, batch: int = 1) -> torch.Tensor:
+                  static_scales: dict[str, float] | None = None, batch: int = 1,
+                  full_act: str = "exact") -> torch.Tensor:
     """transformer.py:443-486: LN2(h + FFC(h)) with h = LN1(x + MHSA(x)).
     Dynamic-activation sites run the fused kernels (LN/GeLU + quantize); the
-    result equals the reference up to attention's float rounding."""
+    result equals the reference up to attention's float rounding.  FullAct sites
+    (A16 schemes, e.g. W8A8/16's attn_in) run igemm.full_linear with
+    `full_act` precision: "exact" (bit-exact sequential f32, CUDA cores) or the
+    tensor-core tolerance modes "f16" / "f16x2"."""
     xt = as_device_f32(x)
     if xt.dim() != 2 or xt.shape[1] != block.dim:
         raise ShapeError(f"block input {tuple(xt.shape)} does not match hidden dim {block.dim}")
@@ -309,9 +313,9 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
         return _act_mode_for(precision, site, layer, static_scales)
 
     am = mode("attn_in")
-    qkv = _linear_site(xt, block.w_qkv, block.b_qkv, am)
+    qkv = _linear_site(xt, block.w_qkv, block.b_qkv, am, full_act)
     ctx = attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], block.num_heads, causal, batch)
-    attn_out = _linear_site(ctx, block.w_o, block.b_o, mode("attn_proj_in"))
+    attn_out = _linear_site(ctx, block.w_o, block.b_o, mode("attn_proj_in"), full_act)
     h = torch.empty_like(xt)
     m_ffc_in = mode("ffc_in")
     if isinstance(m_ffc_in, DynamicAct):
@@ -319,7 +323,7 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
         u = igemm.fused_linear(hq, block.w_h4h, block.b_h4h)
     else:
         igemm.layer_norm_quantize(xt, block.ln1_gamma, block.ln1_beta, 8, LN_EPS, residual=attn_out, ln_out=h)
-        u = _linear_site(h, block.w_h4h, block.b_h4h, m_ffc_in)
+        u = _linear_site(h, block.w_h4h, block.b_h4h, m_ffc_in, full_act)
     m_mid = mode("ffc_mid")
     if isinstance(m_mid, DynamicAct):
         zq = igemm.gelu_quantize(u, 8)
@@ -327,7 +331,7 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
     else:
         z = torch.empty_like(u)
         igemm.gelu_quantize(u, 8, gelu_out=z)
-        f = _linear_site(z, block.w_4hh, block.b_4hh, m_mid)
+        f = _linear_site(z, block.w_4hh, block.b_4hh, m_mid, full_act)
     y = torch.empty_like(xt)
     igemm.layer_norm_quantize(h, block.ln2_gamma, block.ln2_beta, 8, LN_EPS, residual=f, ln_out=y)
     return y

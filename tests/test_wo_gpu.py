@@ -143,3 +143,22 @@ def test_full_precision_validation(zq):
         igemm.full_linear(x, wq, bias, precision="tf32")
     with pytest.raises(UsageError):
         igemm.full_linear(x, wq, bias, precision="exact", out_dtype=torch.float16)
+
+
+@pytest.mark.parametrize("full_act", ["f16", "f16x2"])
+@pytest.mark.parametrize("causal", [False, True])
+def test_block_forward_a16_site_tensor_core(golden, full_act, causal):
+    """W8A8/16 (attn_in is FullAct, transformer.py:395) with the QKV projection on
+    the tensor-core weight-only path: the block output stays within the block
+    tolerance of the reference's golden output (relative L2 2e-3, as the exact
+    path in tests/test_transformer_gpu.py)."""
+    from paper_2206_01861_b200 import transformer as T
+
+    blk = {k[len("block_"):]: v for k, v in golden.items()
+           if k.startswith("block_") and not k.startswith("block_W") and k != "block_x"}
+    blk["num_heads"] = 4
+    prec = T.PrecisionConfig.from_scheme("W8A8/16", hidden_dim=64)
+    db = T.quantize_block(blk, prec)
+    y = T.block_forward(golden["block_x"], db, prec, causal, full_act=full_act).cpu().numpy().astype(np.float64)
+    ref = golden[f"block_W8A8_16_c{int(causal)}_y"].astype(np.float64)
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 2e-3
