@@ -11,6 +11,7 @@
 // value — only float attention (tolerance parity) runs here.
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "zq_common.cuh"
@@ -198,6 +199,188 @@ __global__ void __launch_bounds__(THREADS) decode_attention_kernel(
     ctx[(int64_t)b * ld_ctx + h * dh + i] = t / LL;
   }
   cluster_barrier();  // keep this CTA's partial alive until every peer has read it
+}
+
+// TMA-pipelined variant (the default for head_dim 64 / 96 / 128 / 256): the same
+// cluster-of-C flash-decoding split and merge, but the K and V rows of each
+// CTA's key range stream into a 4-stage shared-memory ring through TMA (one
+// [KT keys x dh] box of each per stage, ~16 KB), so every SM keeps ~200 KB of
+// the cache in flight instead of the ~30 KB of register loads above, which left
+// long contexts (GPT-3 350M: 1030 keys, 67.5 MB per layer) at ~40% of HBM.
+// Warp 4 is the producer; warps 0-3 run the per-virtual-warp online softmax out
+// of shared memory (a key's row is read by LPK consecutive lanes, conflict-free).
+// The key range of a CTA is split from the runtime length lens[b] (not max_ctx),
+// so short contexts keep every CTA busy.
+template <int DH, int KT, int LPK, int NF, int STG_ = 4>
+struct DecTmaCfg {
+  static constexpr int STG = STG_;
+  static constexpr int TILE = KT * DH * 4;            // one K (or V) box
+  static constexpr int SMEM = STG * 2 * TILE + 2 * STG * 8;
+  static constexpr int NVW = 4 * (32 / LPK);          // virtual warps (4 compute warps)
+  static constexpr int KPV = KT / NVW;                // keys per virtual warp per tile
+  static_assert(KT % NVW == 0, "tile must split evenly over the virtual warps");
+};
+
+template <int DH, int KT, int LPK, int NF, int STG_>
+__global__ void __launch_bounds__(160) decode_attention_tma_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+    const float* __restrict__ q, int64_t ld_q, int64_t max_ctx, int heads,
+    const int32_t* __restrict__ lens, float scale, float* __restrict__ ctx, int64_t ld_ctx, int C) {
+  using Cfg = DecTmaCfg<DH, KT, LPK, NF, STG_>;
+  constexpr int NVW = Cfg::NVW, STG = Cfg::STG;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  float* sK = reinterpret_cast<float*>(dsm);
+  float* sV = sK + STG * KT * DH;
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + STG * 2 * Cfg::TILE);
+  uint64_t* empty = full + STG;
+  __shared__ __align__(16) float po[NVW][DH];
+  __shared__ float wst[NVW][2];
+  __shared__ float stat[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    for (int s = 0; s < STG; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  const int c = (int)cta_rank_in_cluster();
+  const int bh = blockIdx.x / C;
+  const int b = bh / heads, h = bh % heads;
+  // lens is written at the start of the step by a non-PDL kernel, so it is
+  // complete before any kernel of the step starts; the cache rows below len - 1
+  // were appended by earlier steps.  Only row len - 1 (this step's k / v, written
+  // by the QKV GEMM that precedes this kernel) and q need the grid dependency:
+  // the producer streams the first tiles that end before that row while the
+  // QKV GEMM drains, then waits.
+  const int len = lens[b];
+  const int per = (((len + C - 1) / C) + KT - 1) / KT * KT;  // keys per CTA, whole tiles
+  const int j0 = c * per, j1 = min(len, j0 + per);
+  const int ntiles = j1 > j0 ? (j1 - j0 + KT - 1) / KT : 0;
+  float m = -INFINITY, l = 0.0f;
+  const int vw = tid / LPK, sl = tid % LPK;
+  float4 o[NF];
+  if (warp == 4) {
+    if (lane == 0) {
+      const int row0 = (int)((int64_t)b * max_ctx) + j0;
+      int t = 0;
+      for (; t < ntiles && t < STG && j0 + (t + 1) * KT <= len - 1; ++t) {
+        mbar_arrive_expect_tx(&full[t], 2 * Cfg::TILE);
+        tma_load_2d(sK + t * KT * DH, &tmK, &full[t], h * DH, row0 + t * KT);
+        tma_load_2d(sV + t * KT * DH, &tmV, &full[t], h * DH, row0 + t * KT);
+      }
+      pdl_wait();
+      for (; t < ntiles; ++t) {
+        const int s = t % STG;
+        if (t >= STG) mbar_wait(&empty[s], ((t / STG) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], 2 * Cfg::TILE);
+        tma_load_2d(sK + s * KT * DH, &tmK, &full[s], h * DH, row0 + t * KT);
+        tma_load_2d(sV + s * KT * DH, &tmV, &full[s], h * DH, row0 + t * KT);
+      }
+    }
+    pdl_wait();
+  } else {
+    pdl_wait();
+    const float sl2 = __fmul_rn(scale, 1.4426950408889634f);
+    const float4* qr = reinterpret_cast<const float4*>(q + (int64_t)b * ld_q + h * DH);
+    float4 qv[NF];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      qv[i] = __ldg(qr + sl + LPK * i);
+      o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % STG;
+      mbar_wait(&full[s], (t / STG) & 1);
+      const float* kt = sK + s * KT * DH;
+      const float* vt = sV + s * KT * DH;
+      float4 kk[Cfg::KPV][NF], vv[Cfg::KPV][NF];
+#pragma unroll
+      for (int u = 0; u < Cfg::KPV; ++u) {
+        const int r = vw + u * NVW;
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+          kk[u][i] = *reinterpret_cast<const float4*>(kt + r * DH + 4 * (sl + LPK * i));
+          vv[u][i] = *reinterpret_cast<const float4*>(vt + r * DH + 4 * (sl + LPK * i));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // the tile is in registers: the slot may refill
+#pragma unroll
+      for (int u = 0; u < Cfg::KPV; ++u) {
+        float d = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+          d = __fmaf_rn(qv[i].x, kk[u][i].x, d);
+          d = __fmaf_rn(qv[i].y, kk[u][i].y, d);
+          d = __fmaf_rn(qv[i].z, kk[u][i].z, d);
+          d = __fmaf_rn(qv[i].w, kk[u][i].w, d);
+        }
+#pragma unroll
+        for (int off = LPK / 2; off > 0; off >>= 1) d = __fadd_rn(d, __shfl_xor_sync(0xffffffffu, d, off));
+        if (j0 + t * KT + vw + u * NVW < j1) {  // keys past len are never touched (the cache there is garbage)
+          const float sv = __fmul_rn(d, sl2);
+          const float mn = fmaxf(m, sv);
+          const float corr = ex2f(__fsub_rn(m, mn));
+          const float pj = ex2f(__fsub_rn(sv, mn));
+          l = __fmaf_rn(l, corr, pj);
+#pragma unroll
+          for (int i = 0; i < NF; ++i) {
+            o[i].x = __fmaf_rn(pj, vv[u][i].x, __fmul_rn(o[i].x, corr));
+            o[i].y = __fmaf_rn(pj, vv[u][i].y, __fmul_rn(o[i].y, corr));
+            o[i].z = __fmaf_rn(pj, vv[u][i].z, __fmul_rn(o[i].z, corr));
+            o[i].w = __fmaf_rn(pj, vv[u][i].w, __fmul_rn(o[i].w, corr));
+          }
+          m = mn;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NF; ++i) *reinterpret_cast<float4*>(&po[vw][4 * (sl + LPK * i)]) = o[i];
+    if (sl == 0) wst[vw][0] = m, wst[vw][1] = l;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < NVW; ++w) M = fmaxf(M, wst[w][0]);
+  float fw[NVW];
+  float L = 0.0f;
+#pragma unroll
+  for (int w = 0; w < NVW; ++w) {
+    fw[w] = wst[w][0] == -INFINITY ? 0.0f : ex2f(__fsub_rn(wst[w][0], M));
+    L = __fmaf_rn(wst[w][1], fw[w], L);
+  }
+  __syncthreads();
+  for (int i = tid; i < DH; i += 160) {
+    float t = 0.0f;
+#pragma unroll
+    for (int w = 0; w < NVW; ++w) t = __fmaf_rn(po[w][i], fw[w], t);
+    po[0][i] = t;
+  }
+  if (tid == 0) stat[0] = M, stat[1] = L;
+  cluster_barrier();
+  const int da = (c * DH) / C, db = ((c + 1) * DH) / C;
+  const uint32_t stat_a = smem_u32(stat), po_a = smem_u32(&po[0][0]);
+  float MM = -INFINITY;
+  for (int r = 0; r < C; ++r) MM = fmaxf(MM, dsm_ld_f32(dsm_map(stat_a, r)));
+  float LL = 0.0f;
+  for (int r = 0; r < C; ++r) {
+    const float mr = dsm_ld_f32(dsm_map(stat_a, r));
+    if (mr != -INFINITY) LL += dsm_ld_f32(dsm_map(stat_a + 4, r)) * ex2f(mr - MM);
+  }
+  for (int i = da + tid; i < db; i += 160) {
+    float t = 0.0f;
+    for (int r = 0; r < C; ++r) {
+      const float mr = dsm_ld_f32(dsm_map(stat_a, r));
+      if (mr != -INFINITY) t += dsm_ld_f32(dsm_map(po_a + 4 * i, r)) * ex2f(mr - MM);
+    }
+    ctx[(int64_t)b * ld_ctx + h * DH + i] = t / LL;
+  }
+  cluster_barrier();
 }
 
 // ---------------------------------------------------------------------------
@@ -502,10 +685,25 @@ int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, 
   return ZQ_OK;
 }
 
+static bool dec_tma_enabled() {
+  static int use_tma = -1;  // ZQ_DEC_TMA=0: the register-load kernel
+  if (use_tma < 0) {
+    const char* ev = getenv("ZQ_DEC_TMA");
+    use_tma = ev ? atoi(ev) : 1;
+  }
+  return use_tma != 0;
+}
+
 int zq_decode_attention_chunks(int batch, int heads, int64_t max_ctx) {
-  // context chunks per (sequence, head): split until ~1000 CTAs of 4 warps are in
-  // flight (7 per SM), at most 8 (portable cluster), keeping >= 16 keys per chunk
+  // context chunks per (sequence, head), at most 8 (portable cluster).  TMA
+  // kernel (measured, tools/dec_attn_bench.py): ~512 CTAs with 2-stage rings,
+  // >= 32 keys per chunk.  Register-load kernel: ~1000 CTAs of 4 warps (7 per
+  // SM), >= 16 keys per chunk.
   int C = 1;
+  if (dec_tma_enabled()) {
+    while (C < 8 && (int64_t)batch * heads * C * 2 <= 512 && max_ctx / (2 * C) >= 32) C *= 2;
+    return C;
+  }
   while (C < 8 && (int64_t)batch * heads * C * 2 <= 7 * 148 && max_ctx / (2 * C) >= 16) C *= 2;
   return C;
 }
@@ -522,6 +720,54 @@ int zq_decode_attention_f32(const float* q, int64_t ld_q, const float* kcache, c
   const int C = chunks ? chunks : zq_decode_attention_chunks(batch, heads, max_ctx);
   const int chunk = (int)((max_ctx + C - 1) / C);
   cudaError_t e;
+  const int64_t dl = (int64_t)heads * head_dim;
+  if (dec_tma_enabled() && (head_dim == 64 || head_dim == 96 || head_dim == 128 || head_dim == 256) &&
+      (reinterpret_cast<uintptr_t>(kcache) & 15) == 0 && (reinterpret_cast<uintptr_t>(vcache) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(q) & 15) == 0 && ld_q % 4 == 0 && (int64_t)batch * max_ctx < (1LL << 31)) {
+    CUtensorMap tk, tv;
+    static int kt64 = -1;  // ZQ_DEC_KT=16: 16-key tiles x 8 stages for head_dim 64 (experiments)
+    if (kt64 < 0) {
+      const char* ev = getenv("ZQ_DEC_KT");
+      kt64 = ev ? atoi(ev) : 32;
+    }
+    const int kt = head_dim == 64 ? (kt64 == 16 ? 16 : 32) : head_dim == 256 ? 8 : 16;
+    static int stg = -1;  // ZQ_DEC_STG: ring stages (2 / 4 / 8)
+    if (stg < 0) {
+      const char* ev = getenv("ZQ_DEC_STG");
+      stg = ev ? atoi(ev) : 2;
+    }
+    int rc = make_tmap_f32(&tk, kcache, (int64_t)batch * max_ctx, dl, dl * 4, head_dim, kt, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc == ZQ_OK)
+      rc = make_tmap_f32(&tv, vcache, (int64_t)batch * max_ctx, dl, dl * 4, head_dim, kt, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc != ZQ_OK) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+#define ZQ_DECT(DH_, KT_, LPK_, NF_, STG_)                                                                 \
+  {                                                                                                         \
+    using Cfg = DecTmaCfg<DH_, KT_, LPK_, NF_, STG_>;                                                       \
+    static ZqDeviceOnce attr_once;                                                                          \
+    attr_once([&](int) {                                                                                    \
+      cudaFuncSetAttribute(decode_attention_tma_kernel<DH_, KT_, LPK_, NF_, STG_>,                          \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);                         \
+    });                                                                                                     \
+    e = launch_kernel(decode_attention_tma_kernel<DH_, KT_, LPK_, NF_, STG_>, dim3(batch * heads * C),      \
+                      dim3(160), Cfg::SMEM, st, C, tk, tv, q, ld_q, max_ctx, heads, lens, scale, ctx,      \
+                      ld_ctx, C);                                                                           \
+  }
+#define ZQ_DECT_S(DH_, KT_, LPK_, NF_) \
+  if (stg == 2) ZQ_DECT(DH_, KT_, LPK_, NF_, 2) else if (stg == 8) ZQ_DECT(DH_, KT_, LPK_, NF_, 8) else ZQ_DECT(DH_, KT_, LPK_, NF_, 4)
+    if (head_dim == 64) {
+      if (kt == 16) { ZQ_DECT_S(64, 16, 16, 1) } else { ZQ_DECT_S(64, 32, 16, 1) }
+    } else if (head_dim == 96) { ZQ_DECT_S(96, 16, 8, 3) }
+    else if (head_dim == 128) { ZQ_DECT_S(128, 16, 32, 1) }
+    else { ZQ_DECT_S(256, 8, 32, 2) }
+#undef ZQ_DECT_S
+#undef ZQ_DECT
+    if (e != cudaSuccess) {
+      set_error("decode attention (tma) launch: %s", cudaGetErrorString(e));
+      return ZQ_ERR_CUDA;
+    }
+    return ZQ_OK;
+  }
 #define ZQ_DEC(TT, LL, NN, UU)                                                                           \
   e = launch_kernel(decode_attention_kernel<TT, LL, NN, UU>, dim3(batch * heads * C), dim3(TT), 0,      \
                     reinterpret_cast<cudaStream_t>(stream), C, q, ld_q, kcache, vcache, max_ctx, heads,  \

@@ -90,6 +90,9 @@ def test_decode_attention_vs_torch():
         vc = torch.randn(batch, max_ctx, dl, device="cuda")
         q = torch.randn(batch, 3 * dl, device="cuda")
         lens = torch.tensor([1, 517, 1041], dtype=torch.int32, device="cuda")
+        for b in range(batch):  # cache rows past a sequence's length are never read (NaN poison)
+            kc[b, int(lens[b]):] = float("nan")
+            vc[b, int(lens[b]):] = float("nan")
         ctx = torch.empty(batch, dl, device="cuda")
         scale = 1.0 / dh ** 0.5
         N.call("zq_decode_attention_f32", q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), max_ctx,

@@ -1,6 +1,6 @@
 """In-graph cost of each kernel family of one GPT decode step (CUDA graph),
 by capturing the step with one family stubbed out:
-python tools/ablate_decode.py [gptj-6b|neox-20b|gpt3-350m]"""
+python tools/ablate_decode.py [gptj-6b|neox-20b|gpt3-350m] [batch prompt]"""
 import os
 import sys
 
@@ -25,17 +25,20 @@ FAMILIES = {
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "gptj-6b"
     cfg = D.CONFIGS[name]
-    eng = D.DecoderEngine(cfg, 16, 256)
-    ids = torch.from_numpy(np.random.default_rng(0).integers(0, cfg.vocab, (16, 128))).cuda()
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+    prompt = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+    eng = D.DecoderEngine(cfg, batch, prompt + 128)
+    ids = torch.from_numpy(np.random.default_rng(0).integers(0, cfg.vocab, (batch, prompt))).cuda()
     eng.prefill(ids)
     torch.cuda.synchronize()
     orig_call, orig_mm, orig_am = N.call, torch.matmul, torch.argmax
 
     def timed(reps=20):
         eng._graph = None
-        eng.pos.fill_(128)
+        eng.pos.fill_(prompt)
+        eng.host_pos = prompt
         eng.step()  # captures
-        eng.pos.fill_(128)
+        eng.pos.fill_(prompt)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -46,7 +49,7 @@ def main():
         return a.elapsed_time(b) / reps * 1e3
 
     base = timed()
-    print(f"{name} decode step: {base:.1f} us")
+    print(f"{name} batch {batch} prompt {prompt} decode step: {base:.1f} us")
     for fam, names in FAMILIES.items():
         N.call = lambda n, *a, _names=names: None if n in _names else orig_call(n, *a)
         try:
