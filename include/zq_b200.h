@@ -240,6 +240,15 @@ int zq_lm_head_argmax(const float* x, int64_t ld_x, int ntok, const float* emb, 
                       float emb_scale, void* xh_ws, void* xl_ws, float* xinv_ws, unsigned long long* keys_ws,
                       int64_t* ids, void* stream);
 
+/* The same head with the embedding pre-split once (zq_lm_embed_split: emb_hi /
+ * emb_lo = f16 hi / lo terms of emb * emb_scale, [vocab, dim] each): the decode
+ * step streams the two f16 terms by TMA with no per-step conversion. */
+int zq_lm_embed_split(const float* emb, int64_t vocab, int64_t dim, float emb_scale, void* emb_hi, void* emb_lo,
+                      void* stream);
+int zq_lm_head_argmax_split(const float* x, int64_t ld_x, int ntok, const void* emb_hi, const void* emb_lo,
+                            int64_t vocab, int64_t dim, float emb_scale, void* xh_ws, void* xl_ws, float* xinv_ws,
+                            unsigned long long* keys_ws, int64_t* ids, void* stream);
+
 /* Diagnostics / tests: the fp32 GeLU estimate the quantizer brackets with, and
  * its per-element relative error bound (x clamped to >= -5.5). */
 int zq_gelu_estimate(const float* x, int64_t n, float* est, float* bound, void* stream);

@@ -59,6 +59,8 @@ _SIGS = {
     "zq_minmax_f32": [_p, _i64, _p, _p, _p],
     "zq_np_expf": [_p, _i64, _p, _p],
     "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
+    "zq_lm_embed_split": [_p, _i64, _i64, _f32, _p, _p, _p],
+    "zq_lm_head_argmax_split": [_p, _i64, _i32, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
     "zq_act_split16": [_p, _i64, _i64, _i64, _i32, _p, _p, _i64, _p, _p, _p],
     "zq_linear_wo": [_p, _p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p],
 }

@@ -14,7 +14,9 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "zq_common.cuh"
+#include <algorithm>
+
+#include "zq_gemm.cuh"
 
 namespace zq {
 
@@ -612,6 +614,158 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc(tmem, 32);
 }
 
+// Pre-split variant: the embedding's f16 hi / lo terms (scaled by the same
+// global power of two) are computed once (zq_lm_embed_split) and streamed by
+// TMA straight into SWIZZLE_128B tiles, so no CUDA-core conversion sits between
+// HBM and the tensor core (4 B per weight element either way).  The tokens'
+// f16 hi / lo k-blocks are TMA-loaded too (after the grid dependency: the prep
+// kernel writes them); the first stages' embedding tiles go out before it.
+// Warps: 0 TMA, 1 MMA, 2-5 epilogue (TMEM logits -> per-token argmax keys).
+constexpr int kLs16 = kLmRows * kLmK * 2;   // one f16 embedding term tile: 16 KB
+constexpr int kLsStage = 2 * kLs16 + 2 * kLmX;
+constexpr int kLsS = 6;
+constexpr int kLsSmem = kLsS * kLsStage + 256;
+
+__global__ void __launch_bounds__(192, 1)
+    lm_head_split_kernel(const __grid_constant__ CUtensorMap tmEh, const __grid_constant__ CUtensorMap tmEl,
+                         const __grid_constant__ CUtensorMap tmXh, const __grid_constant__ CUtensorMap tmXl,
+                         const float* __restrict__ xinv, int ntok, int64_t vocab, int dim, float inv_fe,
+                         unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLsS * kLsStage);
+  uint64_t* full = bars;               // [S] all four tiles landed
+  uint64_t* s_empty = bars + kLsS;     // [S]
+  uint64_t* t_full = bars + 2 * kLsS;  // [2]
+  uint64_t* t_empty = t_full + 2;      // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (int)((vocab + kLmRows - 1) / kLmRows);
+  const int nkb = dim / kLmK;
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    prefetch_tmap(&tmEh);
+    prefetch_tmap(&tmEl);
+    for (int i = 0; i < kLsS; ++i) mbar_init(&full[i], 1), mbar_init(&s_empty[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&t_full[i], 1), mbar_init(&t_empty[i], 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 32);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  if (warp == 0) {
+    if (lane == 0) {
+      // embedding tiles of the first stages before the dependency, token tiles after
+      const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nkb;
+      const int pre = total < kLsS ? total : kLsS;
+      for (int i = 0; i < pre; ++i) {
+        const int tile = blockIdx.x + (i / nkb) * gridDim.x, kb = i % nkb;
+        uint8_t* o = smem + i * kLsStage;
+        mbar_arrive_expect_tx(&full[i], kLsStage);
+        tma_load_2d(o, &tmEh, &full[i], kb * kLmK, tile * kLmRows);
+        tma_load_2d(o + kLs16, &tmEl, &full[i], kb * kLmK, tile * kLmRows);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {
+        const int kb = i % nkb;
+        uint8_t* o = smem + i * kLsStage;
+        tma_load_2d(o + 2 * kLs16, &tmXh, &full[i], kb * kLmK, 0);
+        tma_load_2d(o + 2 * kLs16 + kLmX, &tmXl, &full[i], kb * kLmK, 0);
+      }
+      int st = pre % kLsS, ph = pre / kLsS;
+      for (int i = pre; i < total; ++i) {
+        const int tile = blockIdx.x + (i / nkb) * gridDim.x, kb = i % nkb;
+        mbar_wait(&s_empty[st], ph ^ 1);
+        uint8_t* o = smem + st * kLsStage;
+        mbar_arrive_expect_tx(&full[st], kLsStage);
+        tma_load_2d(o, &tmEh, &full[st], kb * kLmK, tile * kLmRows);
+        tma_load_2d(o + kLs16, &tmEl, &full[st], kb * kLmK, tile * kLmRows);
+        tma_load_2d(o + 2 * kLs16, &tmXh, &full[st], kb * kLmK, 0);
+        tma_load_2d(o + 2 * kLs16 + kLmX, &tmXl, &full[st], kb * kLmK, 0);
+        if (++st == kLsS) st = 0, ph ^= 1;
+      }
+    }
+    pdl_wait();
+  } else if (warp == 1) {
+    pdl_wait();
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(kLmTok >> 3) << 17) | ((uint32_t)(kLmRows >> 4) << 24);
+    int st = 0, ph = 0, acc = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&t_empty[acc], aph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          uint8_t* o = smem + st * kLsStage;
+          const uint64_t dEh = make_sw128_desc(smem_u32(o)), dEl = make_sw128_desc(smem_u32(o + kLs16));
+          const uint64_t dXh = make_sw128_desc(smem_u32(o + 2 * kLs16));
+          const uint64_t dXl = make_sw128_desc(smem_u32(o + 2 * kLs16 + kLmX));
+#pragma unroll
+          for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+            for (int ks = 0; ks < kLmK / 16; ++ks)
+              mma_f16_ss(tmem + acc * 16, (t3 == 2 ? dEl : dEh) + 2 * ks, (t3 == 1 ? dXl : dXh) + 2 * ks, idesc,
+                         (kb | ks | t3) != 0);
+          mma_commit(&s_empty[st]);
+        }
+        __syncwarp();
+        if (++st == kLsS) st = 0, ph ^= 1;
+      }
+      if (lane == 0) mma_commit(&t_full[acc]);
+      __syncwarp();
+      if (++acc == 2) acc = 0, aph ^= 1;
+    }
+  } else {
+    pdl_wait();
+    const int quarter = warp & 3;
+    int acc = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&t_full[acc], aph);
+      tc_fence_after();
+      uint32_t lg[16];
+      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 16, lg);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[acc]);
+      if (++acc == 2) acc = 0, aph ^= 1;
+      const int64_t v = (int64_t)tile * kLmRows + quarter * 32 + lane;
+#pragma unroll
+      for (int t = 0; t < kLmTok; ++t) {
+        if (t >= ntok) break;
+        const float val = __fmul_rn(__fmul_rn(__uint_as_float(lg[t]), inv_fe), xinv[t]);
+        uint32_t u = __float_as_uint(val);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        unsigned long long key = v < vocab ? (((unsigned long long)u << 32) | (0xFFFFFFFFull - (uint64_t)v)) : 0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key, off);
+          key = o2 > key ? o2 : key;
+        }
+        if (lane == 0 && key) atomicMax(keys + t, key);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 32);
+}
+
+// Embedding -> (hi, lo) f16 terms of emb * fe (fe: the caller's power of two).
+__global__ void lm_embed_split_kernel(const float* __restrict__ emb, int64_t n2, float fe, __half* __restrict__ hi,
+                                      __half* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = reinterpret_cast<const float2*>(emb)[i];
+    uint32_t h, l;
+    lm_split(__fmul_rn(v.x, fe), __fmul_rn(v.y, fe), h, l);
+    reinterpret_cast<uint32_t*>(hi)[i] = h;
+    reinterpret_cast<uint32_t*>(lo)[i] = l;
+  }
+}
+
 __global__ void lm_final_kernel(const unsigned long long* __restrict__ keys, int ntok, int64_t* __restrict__ ids) {
   pdl_trigger();
   pdl_wait();
@@ -692,6 +846,57 @@ static bool dec_tma_enabled() {
     use_tma = ev ? atoi(ev) : 1;
   }
   return use_tma != 0;
+}
+
+int zq_lm_embed_split(const float* emb, int64_t vocab, int64_t dim, float emb_scale, void* emb_hi, void* emb_lo,
+                      void* stream) {
+  ZQ_CHECK_ARG(vocab >= 1 && dim >= 2 && dim % 2 == 0, ZQ_ERR_SHAPE, "bad embedding shape");
+  const int64_t n2 = vocab * dim / 2;
+  const int blocks = (int)std::min<int64_t>((n2 + 255) / 256, (int64_t)zq_num_sms() * 16);
+  lm_embed_split_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      emb, n2, emb_scale, reinterpret_cast<__half*>(emb_hi), reinterpret_cast<__half*>(emb_lo));
+  ZQ_LAUNCH_CHECK("embedding split launch");
+  return ZQ_OK;
+}
+
+int zq_lm_head_argmax_split(const float* x, int64_t ld_x, int ntok, const void* emb_hi, const void* emb_lo,
+                            int64_t vocab, int64_t dim, float emb_scale, void* xh_ws, void* xl_ws, float* xinv_ws,
+                            unsigned long long* keys_ws, int64_t* ids, void* stream) {
+  ZQ_CHECK_ARG(ntok >= 1 && ntok <= kLmTok, ZQ_ERR_UNSUPPORTED, "lm head: 1..16 tokens per step");
+  ZQ_CHECK_ARG(dim % kLmK == 0 && vocab >= 1, ZQ_ERR_UNSUPPORTED, "lm head: dim must be a multiple of 64");
+  ZQ_CHECK_ARG((reinterpret_cast<uintptr_t>(emb_hi) & 15) == 0 && (reinterpret_cast<uintptr_t>(emb_lo) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xh_ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(xl_ws) & 15) == 0,
+               ZQ_ERR_USAGE, "lm head operands must be 16-byte aligned");
+  const int nsm = zq_num_sms();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUtensorMap teh, tel, txh, txl;
+  int rc = make_tmap_2d(&teh, CU_TENSOR_MAP_DATA_TYPE_UINT16, emb_hi, vocab, dim, dim * 2, kLmK, kLmRows,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (!rc) rc = make_tmap_2d(&tel, CU_TENSOR_MAP_DATA_TYPE_UINT16, emb_lo, vocab, dim, dim * 2, kLmK, kLmRows,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (!rc) rc = make_tmap_2d(&txh, CU_TENSOR_MAP_DATA_TYPE_UINT16, xh_ws, kLmTok, dim, dim * 2, kLmK, kLmTok,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (!rc) rc = make_tmap_2d(&txl, CU_TENSOR_MAP_DATA_TYPE_UINT16, xl_ws, kLmTok, dim, dim * 2, kLmK, kLmTok,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (rc) return rc;
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
+    cudaFuncSetAttribute(lm_head_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLsSmem);
+  });
+  cudaError_t e = launch_kernel(lm_prep_kernel, dim3(kLmTok), dim3(256), 0, st, 1, x, ld_x, ntok, (int)dim,
+                                reinterpret_cast<__half*>(xh_ws), reinterpret_cast<__half*>(xl_ws), xinv_ws, keys_ws);
+  if (e == cudaSuccess) {
+    const int ntiles = (int)((vocab + kLmRows - 1) / kLmRows);
+    e = launch_kernel(lm_head_split_kernel, dim3(ntiles < nsm ? ntiles : nsm), dim3(192), kLsSmem, st, 1, teh, tel,
+                      txh, txl, (const float*)xinv_ws, ntok, vocab, (int)dim, 1.0f / emb_scale, keys_ws);
+  }
+  if (e == cudaSuccess)
+    e = launch_kernel(lm_final_kernel, dim3(1), dim3(32), 0, st, 1, (const unsigned long long*)keys_ws, ntok, ids);
+  if (e != cudaSuccess) {
+    set_error("lm head (split) launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
 }
 
 int zq_decode_attention_chunks(int batch, int heads, int64_t max_ctx) {

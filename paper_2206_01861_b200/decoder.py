@@ -14,8 +14,9 @@ on the caller side:
 * decode attention for one query row per sequence (zq_decode_attention_f32)
   with the context length in device memory, so one decode step is a fixed
   launch sequence captured once in a CUDA graph;
-* the tied LM head (transformer.py:532) and greedy argmax: float32 logits on
-  tcgen05 (zq_lm_head_argmax: two-term f16 split of the final hidden state,
+* the tied LM head (transformer.py:532) and greedy argmax: float32-accurate
+  logits on tcgen05 (zq_lm_head_argmax_split: the embedding split once into f16
+  hi / lo terms, the final hidden state split per step, three-term products,
   fused argmax) for batch <= 16; torch matmul + argmax above that (the head is
   not on the quantized path);
 * tensor parallelism (tp.py): column-parallel q/k/v/h4h, row-parallel o/4hh
@@ -127,6 +128,15 @@ class DecoderEngine:
         m = float(self.embedding.abs().max())
         self.emb_scale = math.ldexp(1.0, 15 - math.frexp(m)[1]) if m > 0 else 1.0
         self._lm_ok = batch <= 16 and cfg.dim % 64 == 0 and os.environ.get("ZQ_LM_TORCH", "0") != "1"
+        # the embedding's f16 hi / lo terms, split once: each step streams them by TMA
+        # straight into the tensor core (ZQ_LM_SPLIT=0: convert the f32 rows per step)
+        self._emb_split = None
+        if self._lm_ok and os.environ.get("ZQ_LM_SPLIT", "1") != "0":
+            eh = torch.empty((cfg.vocab, cfg.dim), dtype=torch.float16, device=dev)
+            el = torch.empty_like(eh)
+            N.call("zq_lm_embed_split", self.embedding.data_ptr(), cfg.vocab, cfg.dim, self.emb_scale,
+                   eh.data_ptr(), el.data_ptr(), N.stream_ptr())
+            self._emb_split = (eh, el)
         self._lm_ws = dict(xh=torch.zeros(16 * cfg.dim, dtype=torch.float16, device=dev),
                            xl=torch.zeros(16 * cfg.dim, dtype=torch.float16, device=dev),
                            xinv=torch.zeros(16, dtype=torch.float32, device=dev),
@@ -242,7 +252,14 @@ class DecoderEngine:
         self._ln_quant(B["last"], None, self.final_gamma, self.final_beta, B["out"][: self.batch],
                        B["lq"], B["ls"])
         out = B["out"][: self.batch]
-        if self._lm_ok:  # tcgen05 two-term f16 LM head with a fused argmax
+        if self._lm_ok and self._emb_split is not None:  # pre-split embedding, TMA-fed tcgen05 + argmax
+            W = self._lm_ws
+            eh, el = self._emb_split
+            N.call("zq_lm_head_argmax_split", out.data_ptr(), out.stride(0), self.batch, eh.data_ptr(),
+                   el.data_ptr(), self.cfg.vocab, self.cfg.dim, self.emb_scale, W["xh"].data_ptr(),
+                   W["xl"].data_ptr(), W["xinv"].data_ptr(), W["keys"].data_ptr(), self.next_ids.data_ptr(),
+                   N.stream_ptr())
+        elif self._lm_ok:  # tcgen05 two-term f16 LM head with a fused argmax
             W = self._lm_ws
             N.call("zq_lm_head_argmax", out.data_ptr(), out.stride(0), self.batch, self.embedding.data_ptr(),
                    self.cfg.vocab, self.cfg.dim, self.emb_scale, W["xh"].data_ptr(), W["xl"].data_ptr(),

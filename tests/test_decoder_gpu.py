@@ -107,13 +107,15 @@ def test_decode_attention_vs_torch():
             assert torch.allclose(ctx[b].double(), ref, rtol=1e-5, atol=1e-5), (dh, b)
 
 
-def test_lm_head_argmax_vs_f64():
-    """zq_lm_head_argmax (tcgen05 two-term f16 split, fused argmax) vs float64
+@pytest.mark.parametrize("split", [False, True])
+def test_lm_head_argmax_vs_f64(split):
+    """zq_lm_head_argmax (tcgen05 two-term f16 split, fused argmax) and the
+    pre-split variant (zq_lm_embed_split + zq_lm_head_argmax_split) vs float64
     logits: same token wherever the top two logits are not a near-tie; exact ties
     resolve to the lowest index like numpy's argmax."""
     from paper_2206_01861_b200 import _native as N
 
-    for ntok, vocab, dim in ((16, 3001, 256), (5, 50400, 1024), (1, 129, 64)):
+    for ntok, vocab, dim in ((16, 3001, 256), (5, 50400, 1024), (1, 129, 64), (16, 50400, 4096)):
         torch.manual_seed(vocab)
         x = torch.randn(ntok, dim, device="cuda")
         emb = torch.randn(vocab, dim, device="cuda") * 0.02
@@ -125,8 +127,17 @@ def test_lm_head_argmax_vs_f64():
         xinv = torch.zeros(16, device="cuda")
         keys = torch.zeros(16, dtype=torch.int64, device="cuda")
         ids = torch.full((ntok,), -1, dtype=torch.int64, device="cuda")
-        N.call("zq_lm_head_argmax", x.data_ptr(), x.stride(0), ntok, emb.data_ptr(), vocab, dim, scale,
-               xh.data_ptr(), xl.data_ptr(), xinv.data_ptr(), keys.data_ptr(), ids.data_ptr(), N.stream_ptr())
+        if split:
+            eh = torch.empty(vocab, dim, dtype=torch.float16, device="cuda")
+            el = torch.empty_like(eh)
+            N.call("zq_lm_embed_split", emb.data_ptr(), vocab, dim, scale, eh.data_ptr(), el.data_ptr(),
+                   N.stream_ptr())
+            N.call("zq_lm_head_argmax_split", x.data_ptr(), x.stride(0), ntok, eh.data_ptr(), el.data_ptr(), vocab,
+                   dim, scale, xh.data_ptr(), xl.data_ptr(), xinv.data_ptr(), keys.data_ptr(), ids.data_ptr(),
+                   N.stream_ptr())
+        else:
+            N.call("zq_lm_head_argmax", x.data_ptr(), x.stride(0), ntok, emb.data_ptr(), vocab, dim, scale,
+                   xh.data_ptr(), xl.data_ptr(), xinv.data_ptr(), keys.data_ptr(), ids.data_ptr(), N.stream_ptr())
         logits = x.double() @ emb.double().t()
         top2 = logits.topk(2, dim=1)
         ref = logits.argmax(dim=1)

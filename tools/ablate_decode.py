@@ -18,7 +18,7 @@ FAMILIES = {
     "ln": ("zq_layer_norm_quantize",),
     "gelu": ("zq_gelu_quantize",),
     "tok": ("zq_quantize_tokenwise",),
-    "lm_head": ("zq_lm_head_argmax",),
+    "lm_head": ("zq_lm_head_argmax", "zq_lm_head_argmax_split"),
 }
 
 
