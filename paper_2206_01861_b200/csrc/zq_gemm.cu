@@ -591,8 +591,14 @@ __device__ __forceinline__ int32_t dsmem_ld_s32(uint32_t addr) {
 // W4: TMA brings the packed nibbles ([128 rows x 64 B], unswizzled) and warps 2-3
 // (idle during the main loop otherwise) unpack them into the int8 SWIZZLE_128B
 // tile the MMA reads, then add their arrivals on the stage's full barrier.
+// W4: 256 threads (warps 2-7 unpack: the INT4 -> INT8 expansion of a 16 KB
+// k-block by 64 threads left the 4hh projection of GPT-3 350M decode (4 k-blocks
+// per CTA) unpack-bound); the TMEM partial / reduction use warps 0-3 / all.
+template <int MP, int W4>
+constexpr int skinny_threads() { return W4 ? 256 : 128; }
+
 template <int MP, int KIND, int W4>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(skinny_threads<MP, W4>(), 1)
     zq_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                           const GemmParams p, int S) {
   using Cfg = SkinnyCfg<MP, W4>;
@@ -619,7 +625,7 @@ __global__ void __launch_bounds__(128, 1)
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     for (int st = 0; st < kSkStages; ++st) {
-      mbar_init(&full_bar[st], W4 ? 3 : 1);  // W4: + one arrival per unpack warp
+      mbar_init(&full_bar[st], W4 ? 1 + (skinny_threads<MP, W4>() / 32 - 2) : 1);  // W4: + one arrival per unpack warp
       mbar_init(&empty_bar[st], 1);
       if (W4) mbar_init(&praw_bar[st], 1);
     }
@@ -692,6 +698,7 @@ __global__ void __launch_bounds__(128, 1)
   } else if (W4) {
     // warps 2-3: INT4 -> INT8 into the SWIZZLE_128B tile (row r, 16-byte chunk c at
     // r*128 + ((c ^ (r & 7)) * 16)); nibble j of a packed word is element j
+    constexpr int UT = skinny_threads<MP, W4>() - 64;  // unpack threads
     const int ut = threadIdx.x - 64;
     int stage = 0, phase = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
@@ -699,8 +706,8 @@ __global__ void __launch_bounds__(128, 1)
       mbar_wait(&praw_bar[stage], phase);
       const uint8_t* src = sP + stage * Cfg::P_BYTES;
       uint8_t* dst = sA + stage * Cfg::A_BYTES;
-#pragma unroll 4
-      for (int idx = ut; idx < 128 * 8; idx += 64) {
+#pragma unroll 2
+      for (int idx = ut; idx < 128 * 8; idx += UT) {
         const int rr = idx >> 3, c = idx & 7;
         const uint2 pk = *reinterpret_cast<const uint2*>(src + rr * 64 + c * 8);
         uint32_t w[4];
@@ -727,14 +734,16 @@ __global__ void __launch_bounds__(128, 1)
   // ---- partial: TMEM (lane = weight row) -> smem [MP][128] ----
   mbar_wait(done_bar, 0);
   tc_fence_after();
-  const int row = warp * 32 + lane;
+  if (warp < 4) {
+    const int row = warp * 32 + lane;
 #pragma unroll
-  for (int c = 0; c < MP; c += 32) {
-    uint32_t v[32];
-    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
-    tmem_ld_wait();
+    for (int c = 0; c < MP; c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+      tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) part[(c + j) * 128 + row] = kb1 > kb0 ? (int32_t)v[j] : 0;
+      for (int j = 0; j < 32; ++j) part[(c + j) * 128 + row] = kb1 > kb0 ? (int32_t)v[j] : 0;
+    }
   }
   tc_fence_before();
   pdl_wait();
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(128, 1)
   // ---- cluster reduction + epilogue for rows [128 r / S, 128 (r+1) / S) ----
   const int r_lo = (128 * r) / S, RP = (128 * (r + 1)) / S - r_lo;
   const uint32_t pbase = smem_u32(part);
-  for (int it = threadIdx.x; it < MP * RP; it += 128) {
+  for (int it = threadIdx.x; it < MP * RP; it += skinny_threads<MP, W4>()) {
     const int m = it / RP, nl = r_lo + it % RP;
     const int n = n0 + nl;
     if (m >= p.M || n >= p.N) continue;
@@ -1414,7 +1423,8 @@ static int launch_skinny_t(const CUtensorMap& tw, const CUtensorMap& tx, GemmPar
     cudaFuncSetAttribute(zq_gemm_skinny_kernel<MP, KIND, W4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
   });
-  cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND, W4>, dim3(p.num_n_tiles * S), dim3(128),
+  cudaError_t e = launch_kernel(zq_gemm_skinny_kernel<MP, KIND, W4>, dim3(p.num_n_tiles * S),
+                                dim3(skinny_threads<MP, W4>()),
                                 Cfg::SMEM_BYTES, st, S, tw, tx, p, S);
   if (e != cudaSuccess) {
     set_error("skinny gemm launch: %s", cudaGetErrorString(e));
