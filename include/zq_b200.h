@@ -195,6 +195,18 @@ int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int h
 int zq_kv_append(const float* qkv, int64_t ld_qkv, int batch, int rows_per_seq, int dmodel_local,
                  const int32_t* pos, float* kcache, float* vcache, int64_t max_ctx, void* stream);
 
+/* zq_linear with a caller-owned int32 workspace for decode-sized calls (M <= 64,
+ * int8 weights): the stream-K skinny kernel (k-block units split evenly over
+ * two CTAs per SM, exact int32 partial sums added in the workspace, then a
+ * light dequant-epilogue kernel that also re-zeroes it).  The workspace
+ * (zq_linear_ws_bytes(M, N) bytes, 16-byte aligned) must be zeroed once before
+ * first use; every launch leaves it zeroed.  Other shapes: exactly zq_linear. */
+int64_t zq_linear_ws_bytes(int64_t M, int64_t N);
+int zq_linear_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, float static_scale, const void* wq,
+                 int64_t ld_w, int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N,
+                 int64_t K, void* out, int64_t ld_out, int out_type, void* workspace, int64_t workspace_bytes,
+                 void* stream);
+
 /* Decode QKV projection with the KV-cache append fused into the epilogue: as
  * zq_linear (f32 output, M <= 64 rows, one row per sequence) and additionally
  * kcache / vcache[m, pos[m], :] = columns [dl, 2 dl) / [2 dl, 3 dl) of row m
@@ -204,6 +216,11 @@ int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, cons
                  int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
                  float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
                  int64_t max_ctx, void* stream);
+/* The same with the stream-K workspace (see zq_linear_ws). */
+int zq_linear_kv_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                    int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                    float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
+                    int64_t max_ctx, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* One-token-per-sequence attention against the caches (transformer.py:413-440
  * for the last query row): ctx[b, h] = softmax(q.K^T * scale) V over the first

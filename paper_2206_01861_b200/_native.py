@@ -61,6 +61,9 @@ _SIGS = {
     "zq_lm_head_argmax": [_p, _i64, _i32, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
     "zq_lm_embed_split": [_p, _i64, _i64, _f32, _p, _p, _p],
     "zq_lm_head_argmax_split": [_p, _i64, _i32, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
+    "zq_linear_ws": [_p, _i64, _p, _f32, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p, _i64, _p],
+    "zq_linear_kv_ws": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i32, _i64,
+                        _p, _i64, _p],
     "zq_act_split16": [_p, _i64, _i64, _i64, _i32, _p, _p, _i64, _p, _p, _p],
     "zq_linear_wo": [_p, _p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p],
 }
@@ -74,7 +77,7 @@ class NativeUnavailable(RuntimeError):
 
 
 def exported_symbols() -> list[str]:
-    return sorted(_SIGS) + ["zq_version", "zq_last_error"]
+    return sorted(_SIGS) + ["zq_version", "zq_last_error", "zq_linear_ws_bytes"]
 
 
 def load(require_device: bool = True):
@@ -99,6 +102,8 @@ def load(require_device: bool = True):
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
+        lib.zq_linear_ws_bytes.argtypes = [_i64, _i64]
+        lib.zq_linear_ws_bytes.restype = ctypes.c_int64
         lib.zq_version.restype = ctypes.c_char_p
         lib.zq_last_error.restype = ctypes.c_char_p
         _lib = lib

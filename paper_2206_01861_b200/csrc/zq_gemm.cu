@@ -785,6 +785,162 @@ __global__ void __launch_bounds__(skinny_threads<MP, W4>(), 1)
 
 
 // ---------------------------------------------------------------------------
+// Stream-K skinny (decode) GEMM, M <= 64 tokens, int8 weights.  The cluster
+// split-K kernel above gives every CTA one (n-tile, k-range) of equal size, so a
+// grid of 1.3 waves (NeoX h4h: 384 CTAs on 296 slots) streams at ~70% of HBM.
+// Here the n_tiles x nkb k-block units are cut into G = 2 x #SMs equal
+// contiguous ranges (tile-major); a CTA accumulates each tile segment of its
+// range in TMEM (swap-AB, double-buffered) and adds it to an int32 workspace
+// with red.global.add (exact: integer addition is order-free).  The dequant
+// epilogue runs as the next kernel (skinny_sum_epilogue_kernel), which also
+// re-zeroes the workspace: a last-arriver epilogue inside this kernel (counter +
+// gpu-scope fences) measured ~8 us slower per launch at NeoX widths, the fences
+// stalling the CTA's in-flight weight stream (tools/skinny_bench.py).
+//   warp 0 TMA (weights of the first stages before the grid dependency),
+//   warp 1 MMA, warps 2-5 reduction (TMEM lane quarters 2, 3, 0, 1).
+constexpr int kSkkStages = 4;  // 80 KB per CTA, two CTAs per SM
+
+template <int MP>
+struct StreamKCfg {
+  static constexpr int A_BYTES = 128 * BLOCK_K;
+  static constexpr int B_BYTES = MP * BLOCK_K;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = kSkkStages * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int MP, int KIND>
+__global__ void __launch_bounds__(192, 2)
+    zq_gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                           const GemmParams p) {
+  using Cfg = StreamKCfg<MP>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kSkkStages * Cfg::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSkkStages * Cfg::STAGE_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + kSkkStages;
+  uint64_t* tfull_bar = bars + 2 * kSkkStages;      // [2]
+  uint64_t* tempty_bar = bars + 2 * kSkkStages + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kSkkStages + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = p.num_k_blocks, ntile = p.num_n_tiles;
+  const int64_t U = (int64_t)ntile * nkb;
+  const int u0 = (int)(U * blockIdx.x / gridDim.x), u1 = (int)(U * (blockIdx.x + 1) / gridDim.x);
+  int32_t* acc_ws = p.sk_ws;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int st = 0; st < kSkkStages; ++st) {
+      mbar_init(&full_bar[st], 1);
+      mbar_init(&empty_bar[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  __syncwarp();
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * MP);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int pre = (u1 - u0) < kSkkStages ? (u1 - u0) : kSkkStages;
+      for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
+        const int u = u0 + i;
+        mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
+        tma_load_2d(sA + i * Cfg::A_BYTES, &tmW, &full_bar[i], (u % nkb) * BLOCK_K, (u / nkb) * 128);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sB + i * Cfg::B_BYTES, &tmX, &full_bar[i], ((u0 + i) % nkb) * BLOCK_K, 0);
+      int stage = pre % kSkkStages, phase = pre / kSkkStages;
+      for (int u = u0 + pre; u < u1; ++u) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        tma_load_2d(sA + stage * Cfg::A_BYTES, &tmW, &full_bar[stage], (u % nkb) * BLOCK_K, (u / nkb) * 128);
+        tma_load_2d(sB + stage * Cfg::B_BYTES, &tmX, &full_bar[stage], (u % nkb) * BLOCK_K, 0);
+        if (++stage == kSkkStages) stage = 0, phase ^= 1;
+      }
+    }
+    pdl_wait();
+  } else if (warp == 1) {
+    pdl_wait();
+    constexpr uint32_t idesc = make_idesc_i8(128, MP);
+    int stage = 0, phase = 0, acc = 0, aph = 0;
+    for (int u = u0; u < u1;) {
+      const int tile = u / nkb, uend = min(u1, (tile + 1) * nkb);
+      mbar_wait(&tempty_bar[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * MP;
+      for (int v = u; v < uend; ++v) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BLOCK_K / 32; ++k)
+            mma_i8(d, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32), idesc,
+                   (v != u || k != 0) ? 1u : 0u);
+          mma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == kSkkStages) stage = 0, phase ^= 1;
+      }
+      if (lane == 0) mma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) acc = 0, aph ^= 1;
+      u = uend;
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM lane quarter q = warp & 3 (rows 32q .. 32q+31) =====
+    pdl_wait();
+    const int q = warp & 3;
+    const int nl = q * 32 + lane;     // this thread's weight row of the tile
+    int acc = 0, aph = 0;
+    for (int u = u0; u < u1;) {
+      const int tile = u / nkb, uend = min(u1, (tile + 1) * nkb);
+      mbar_wait(&tfull_bar[acc], aph);
+      tc_fence_after();
+      uint32_t r[MP];
+#pragma unroll
+      for (int c = 0; c < MP; c += 32) {
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + acc * MP + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) acc = 0, aph ^= 1;
+      const int mlim = p.M < MP ? p.M : MP;
+      // this segment's partial -> the tile's int32 sums (red.add: exact, order-free);
+      // the dequant epilogue is the next kernel (skinny_sum_epilogue_kernel)
+      int32_t* tw = acc_ws + (int64_t)tile * MP * 128;
+#pragma unroll
+      for (int m = 0; m < MP; ++m)
+        if (m < mlim) red_add_s32(tw + m * 128 + nl, (int32_t)r[m]);
+      u = uend;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 2 * MP);
+}
+
+// ---------------------------------------------------------------------------
 // Fused row-parallel projection + residual + LayerNorm + token-wise quantize
 // (transformer.py:474-477 / :484-486: y = LN(x + linear(q, w)), igemm.py:150-157):
 //   f  = ((f32(acc) * s_tok) * s_w) + bias      (igemm.py:107-111, exact order)
@@ -1448,6 +1604,112 @@ static int pick_split(int n_tiles, int nkb) {
   return S;
 }
 
+// out[m, n] = ((f32(S[n / 128][m][n % 128]) * s_tok[m]) * s_w[n]) + b[n] (igemm.py:107-111,
+// strict order) from the stream-K sums, + the fused KV-cache append of the decode
+// QKV projection; every sum is re-zeroed for the next launch.
+template <int KIND>
+__device__ __forceinline__ void sum_epi_store(const GemmParams& p, int m, int n, const int32_t (&a)[4], float st,
+                                              const float4& w, const float4& bb) {
+  const int64_t o = (int64_t)m * p.ld_out + n;
+  if (KIND == OUT_S32) {
+    *reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(p.out) + o) = make_int4(a[0], a[1], a[2], a[3]);
+    return;
+  }
+  const float wv[4] = {w.x, w.y, w.z, w.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+  float f[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    f[j] = __fmul_rn(__fmul_rn(__int2float_rn(a[j]), st), wv[j]);
+    if (p.bias) f[j] = __fadd_rn(f[j], bv[j]);
+  }
+  if (KIND == OUT_F32) {
+    const float4 v = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o) = v;
+    if (p.kc != nullptr && n >= p.kv_dl) {  // fused KV-cache append (decode QKV); dl % 4 == 0
+      const int64_t slot = ((int64_t)m * p.kv_max_ctx + p.kv_pos[m]) * p.kv_dl;
+      if (n < 2 * p.kv_dl) *reinterpret_cast<float4*>(p.kc + slot + (n - p.kv_dl)) = v;
+      else *reinterpret_cast<float4*>(p.vc + slot + (n - 2 * p.kv_dl)) = v;
+    }
+  } else if (KIND == OUT_F16) {
+    __half2 h0 = __floats2half2_rn(f[0], f[1]), h1 = __floats2half2_rn(f[2], f[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&h0);
+    u.y = *reinterpret_cast<uint32_t*>(&h1);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.out) + o) = u;
+  } else {
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(f[0], f[1]), h1 = __floats2bfloat162_rn(f[2], f[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&h0);
+    u.y = *reinterpret_cast<uint32_t*>(&h1);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o) = u;
+  }
+}
+
+// out[m, n] = ((f32(S[n / 128][m][n % 128]) * s_tok[m]) * s_w[n]) + b[n] (igemm.py:107-111,
+// strict order) from the stream-K sums, + the fused KV-cache append of the decode
+// QKV projection; every sum is re-zeroed for the next launch.  One thread per 4
+// consecutive columns of a row (all loads independent: one L2 round trip).
+template <int KIND>
+__global__ void __launch_bounds__(256) skinny_sum_epilogue_kernel(int32_t* __restrict__ ws, int mp, GemmParams p) {
+  pdl_trigger();
+  pdl_wait();
+  const int n4 = p.N >> 2;
+  const int total = p.M * n4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int m = i / n4, n = (i - m * n4) * 4;
+    int4* sp = reinterpret_cast<int4*>(ws + ((int64_t)(n >> 7) * mp + m) * 128 + (n & 127));
+    const int4 a4 = __ldcg(sp);
+    const float st = p.token_scales ? __ldg(p.token_scales + m) : p.static_scale;
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f), bb = w;
+    if (KIND != OUT_S32) {
+      w = __ldg(reinterpret_cast<const float4*>(p.row_scales + n));
+      if (p.bias) bb = __ldg(reinterpret_cast<const float4*>(p.bias + n));
+    }
+    *sp = make_int4(0, 0, 0, 0);
+    const int32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
+    sum_epi_store<KIND>(p, m, n, a, st, w, bb);
+  }
+}
+
+template <int MP, int KIND>
+static int launch_streamk_t(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int grid,
+                            cudaStream_t st) {
+  using Cfg = StreamKCfg<MP>;
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
+    cudaFuncSetAttribute(zq_gemm_streamk_kernel<MP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
+  });
+  cudaError_t e = launch_kernel(zq_gemm_streamk_kernel<MP, KIND>, dim3(grid), dim3(192), Cfg::SMEM_BYTES, st, 1, tw,
+                                tx, p);
+  static int noepi = -1;  // diagnostics: ZQ_SK_NOEPI=1 skips the epilogue kernel (wrong results)
+  if (noepi < 0) noepi = getenv("ZQ_SK_NOEPI") ? 1 : 0;
+  if (e == cudaSuccess && !noepi) {
+    const int64_t total = (int64_t)p.M * (p.N / 4);
+    const int eg = (int)std::min<int64_t>((total + 255) / 256, (int64_t)zq_num_sms() * 8);
+    e = launch_kernel(skinny_sum_epilogue_kernel<KIND>, dim3(eg), dim3(256), 0, st, 1, p.sk_ws, MP, p);
+  }
+  if (e != cudaSuccess) {
+    set_error("stream-K skinny gemm launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+int64_t streamk_ws_bytes(int64_t M, int64_t N) {
+  const int64_t nt = (N + 127) / 128, mp = M <= 32 ? 32 : 64;
+  return 4 * nt * mp * 128;
+}
+
+static int sk_min_bytes() {
+  static int v = -1;  // ZQ_GEMM_STREAMK_MIN: weight bytes from which decode GEMMs go stream-K
+  if (v < 0) {
+    const char* e = getenv("ZQ_GEMM_STREAMK_MIN");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits, int64_t M,
                        int64_t N, int64_t K, int kind, GemmParams p, cudaStream_t st) {
   const int MP = M <= 32 ? 32 : 64;
@@ -1463,6 +1725,40 @@ static int gemm_skinny(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
   p.num_n_tiles = (int)((N + 127) / 128);
   p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
   p.num_tiles = p.num_n_tiles;
+  static int sk_mode = -1;  // ZQ_GEMM_STREAMK=0: the cluster split-K kernel even with a workspace
+  if (sk_mode < 0) {
+    const char* e = getenv("ZQ_GEMM_STREAMK");
+    sk_mode = e ? atoi(e) : 1;
+  }
+  // stream-K pays an extra (epilogue) launch; measured at GPT-J / NeoX decode it wins
+  // at every width (GPT-J o 16.8 MB: 7.2 -> 6.2 us; NeoX h4h 151 MB: 33.8 -> 30.9 us,
+  // tools/skinny_bench.py).  ZQ_GEMM_STREAMK_MIN (bytes) keeps smaller GEMMs on the
+  // cluster split-K kernel.
+  const bool sk_big = (int64_t)N * K >= (int64_t)sk_min_bytes();
+  const int osz = (kind == OUT_F16 || kind == OUT_BF16) ? 2 : 4;
+  const bool sk_aligned = N % 4 == 0 && (p.ld_out * osz) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(p.row_scales) & 15) == 0 &&
+                          (p.bias == nullptr || (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0) &&
+                          (p.kc == nullptr || (p.kv_dl % 4 == 0 && (reinterpret_cast<uintptr_t>(p.kc) & 15) == 0 &&
+                                               (reinterpret_cast<uintptr_t>(p.vc) & 15) == 0));
+  if (w_bits == 8 && p.sk_ws != nullptr && sk_mode != 0 && sk_big && sk_aligned &&
+      p.sk_ws_bytes >= streamk_ws_bytes(M, N) && (reinterpret_cast<uintptr_t>(p.sk_ws) & 15) == 0) {
+    const int64_t units = (int64_t)p.num_n_tiles * p.num_k_blocks;
+    static int sk_cps = -1;  // ZQ_GEMM_STREAMK_CPS: CTAs per SM (memory-level parallelism)
+    if (sk_cps < 0) {
+      const char* e = getenv("ZQ_GEMM_STREAMK_CPS");
+      sk_cps = e ? atoi(e) : 2;
+    }
+    const int grid = (int)std::min<int64_t>(units, (int64_t)zq_num_sms() * sk_cps);
+#define ZQ_SKK(KK) (MP == 32 ? launch_streamk_t<32, KK>(tw, tx, p, grid, st) : launch_streamk_t<64, KK>(tw, tx, p, grid, st))
+    switch (kind) {
+      case OUT_S32: return ZQ_SKK(OUT_S32);
+      case OUT_F32: return ZQ_SKK(OUT_F32);
+      case OUT_F16: return ZQ_SKK(OUT_F16);
+      default: return ZQ_SKK(OUT_BF16);
+    }
+#undef ZQ_SKK
+  }
   const int S = pick_split(p.num_n_tiles, p.num_k_blocks);
 #define ZQ_SK(KK)                                                                               \
   (w_bits == 4 ? (MP == 32 ? launch_skinny_t<32, KK, 1>(tw, tx, p, S, st) : launch_skinny_t<64, KK, 1>(tw, tx, p, S, st)) \
@@ -1732,10 +2028,39 @@ int zq_linear(const int8_t* xq, int64_t ld_x, const float* token_scales, float s
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
+int64_t zq_linear_ws_bytes(int64_t M, int64_t N) { return streamk_ws_bytes(M, N); }
+
+int zq_linear_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, float static_scale, const void* wq,
+                 int64_t ld_w, int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N,
+                 int64_t K, void* out, int64_t ld_out, int out_type, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
+  ZQ_CHECK_ARG(out_type >= ZQ_OUT_F32 && out_type <= ZQ_OUT_BF16, ZQ_ERR_USAGE, "bad output type %d", out_type);
+  ZQ_CHECK_ARG(w_row_scales != nullptr, ZQ_ERR_USAGE, "fused linear needs weight scales");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.out = out;
+  p.ld_out = ld_out;
+  p.token_scales = token_scales;
+  p.static_scale = static_scale;
+  p.row_scales = w_row_scales;
+  p.bias = bias;
+  p.sk_ws = reinterpret_cast<int32_t*>(workspace);
+  p.sk_ws_bytes = workspace_bytes;
+  return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, out_type + 1, p, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
                  int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
                  float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
                  int64_t max_ctx, void* stream) {
+  return zq_linear_kv_ws(xq, ld_x, token_scales, wq, ld_w, w_bits, w_row_scales, bias, M, N, K, out, ld_out, kcache,
+                         vcache, pos, dmodel_local, max_ctx, nullptr, 0, stream);
+}
+
+int zq_linear_kv_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                    int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                    float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
+                    int64_t max_ctx, void* workspace, int64_t workspace_bytes, void* stream) {
   ZQ_CHECK_ARG(w_row_scales != nullptr && kcache && vcache && pos, ZQ_ERR_USAGE, "linear + kv append needs every operand");
   ZQ_CHECK_ARG(N == 3LL * dmodel_local && ld_out >= N, ZQ_ERR_SHAPE, "qkv output must be 3 x dmodel_local wide");
   static int skinny_mode = -1;
@@ -1756,6 +2081,8 @@ int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, cons
   p.kv_pos = pos;
   p.kv_dl = dmodel_local;
   p.kv_max_ctx = max_ctx;
+  p.sk_ws = reinterpret_cast<int32_t*>(workspace);
+  p.sk_ws_bytes = workspace_bytes;
   return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, OUT_F32, p, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -38,6 +38,10 @@ struct GemmParams {
   const int32_t* kv_pos;
   int kv_dl;
   int64_t kv_max_ctx;
+  // decode stream-K (skinny, W8): zero-initialised int32 workspace of per-tile
+  // partial sums, left zeroed by every launch (nullable)
+  int32_t* sk_ws;
+  int64_t sk_ws_bytes;
 };
 
 __device__ __forceinline__ void bulk_wait_read1() {

@@ -144,6 +144,11 @@ class DecoderEngine:
         # decode-attention context chunking planned for the UNSHARDED head count:
         # the float merge order then does not depend on the TP degree
         self._dec_chunks = int(N.load().zq_decode_attention_chunks(batch, cfg.heads, max_ctx))
+        # stream-K decode GEMMs (zq_linear_ws): one zero-initialised int32 workspace
+        # shared by every decode-step linear (each launch leaves it zeroed)
+        lib = N.load()
+        wsb = max(int(lib.zq_linear_ws_bytes(batch, n)) for n in (3 * self.dl, cfg.dim, self.fl))
+        self._sk_ws = torch.zeros(wsb // 4 + 4, dtype=torch.int32, device=dev)
         self._bufs: dict[int, dict] = {}
         self._graph = None
         self.scale = float(np.float32(1.0 / math.sqrt(cfg.head_dim)))
@@ -170,19 +175,20 @@ class DecoderEngine:
     def _linear(self, q, s, w, bias, out, bias_on=True):
         t, k = q.shape
         wp, ldw, wb = w.weight_operand()
-        N.call("zq_linear", q.data_ptr(), q.stride(0), s.data_ptr(), 0.0, wp, ldw, wb,
+        N.call("zq_linear_ws", q.data_ptr(), q.stride(0), s.data_ptr(), 0.0, wp, ldw, wb,
                w.row_scales().data_ptr(), N.ptr(bias) if bias_on else None, t, w.rows, k,
-               out.data_ptr(), out.stride(0), N.OUT_F32, N.stream_ptr())
+               out.data_ptr(), out.stride(0), N.OUT_F32, self._sk_ws.data_ptr(), 4 * self._sk_ws.numel(),
+               N.stream_ptr())
 
     def _qkv_kv(self, xq, sx, blk, qkv, li: int, t: int) -> bool:
         """Decode step: QKV linear with the KV-cache append in its epilogue
         (zq_linear_kv); False when unsupported (the caller appends separately)."""
         w = blk.w_qkv
         wp, ldw, wb = w.weight_operand()
-        rc = N.call_rc("zq_linear_kv", xq.data_ptr(), xq.stride(0), sx.data_ptr(), wp, ldw, wb,
+        rc = N.call_rc("zq_linear_kv_ws", xq.data_ptr(), xq.stride(0), sx.data_ptr(), wp, ldw, wb,
                        w.row_scales().data_ptr(), blk.b_qkv.data_ptr(), t, w.rows, xq.shape[1], qkv.data_ptr(),
                        qkv.stride(0), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(), self.pos.data_ptr(),
-                       self.dl, self.max_ctx, N.stream_ptr())
+                       self.dl, self.max_ctx, self._sk_ws.data_ptr(), 4 * self._sk_ws.numel(), N.stream_ptr())
         return rc != N.ZQ_ERR_UNSUPPORTED
 
     def _tok_quant(self, x, q, s):

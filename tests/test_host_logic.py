@@ -105,7 +105,7 @@ def test_library_exports_every_header_symbol():
         pytest.skip("library not built (run __graft_entry__.build())")
     with open(os.path.join(ROOT, "include", "zq_b200.h")) as f:
         header = f.read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(zq_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(zq_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     lib = _native.load_for_inspection()
     for sym in declared:

@@ -271,3 +271,38 @@ def test_skinny_decode_gemm_w4_exact(zq, shape):
     assert np.array_equal(h(acc.acc), ref_acc), shape
     out = igemm.fused_linear(xa, wm, None)
     assert bits_eq(h(out), O.dequant_epilogue(ref_acc, h(xa.token_scales), np.full(n, F32(0.01)), None)), shape
+
+
+@pytest.mark.parametrize("shape", [(16, 4096, 12288), (16, 6144, 24576), (16, 24576, 6144), (1, 4096, 4096),
+                                   (33, 6144, 3000), (8, 1024, 3072), (64, 768, 768), (3, 200, 300)])
+def test_streamk_decode_gemm_exact(zq, shape):
+    """zq_linear_ws (M <= 64, int8 weights): the stream-K skinny kernel (k-block
+    units split evenly over the SMs, int32 partials added in a workspace, the
+    last contributor of a tile dequantizes) is bit-exact, over repeated launches
+    on one workspace (each launch must leave it zeroed), for f32 and f16 outputs."""
+    from paper_2206_01861_b200 import _native as N
+
+    quant, igemm = zq
+    t, d, n = shape
+    rng = np.random.default_rng(sum(shape) + 7)
+    xv = rng.integers(-127, 128, (t, d)).astype(np.int8)
+    wv = rng.integers(-127, 128, (n, d)).astype(np.int8)
+    xa, wm = make_qact(quant, xv, scales=rng.random(t).astype(F32) + 0.01), make_qmat(quant, wv, scales=(0.003,))
+    bias = torch.from_numpy(rng.standard_normal(n).astype(F32)).cuda()
+    ref_acc = O.igemm(xv, wv)
+    ref = O.dequant_epilogue(ref_acc, h(xa.token_scales), np.full(n, F32(0.003)), h(bias))
+    nbytes = int(N.load().zq_linear_ws_bytes(t, n))
+    ws = torch.zeros(nbytes // 4, dtype=torch.int32, device="cuda")
+    a = xa.gemm_operand()
+    wp, ldw, wb = wm.weight_operand()
+    for it in range(3):
+        for dt, code in ((torch.float32, N.OUT_F32), (torch.float16, N.OUT_F16)):
+            out = torch.empty(t, n, dtype=dt, device="cuda")
+            N.call("zq_linear_ws", a.data_ptr(), a.stride(0), xa.token_scales.data_ptr(), 0.0, wp, ldw, wb,
+                   wm.row_scales().data_ptr(), bias.data_ptr(), t, n, d, out.data_ptr(), out.stride(0), code,
+                   ws.data_ptr(), nbytes, N.stream_ptr())
+            if dt == torch.float32:
+                assert bits_eq(h(out), ref), (shape, it)
+            else:
+                assert torch.equal(out.cpu(), torch.from_numpy(ref).half()), (shape, it)
+            assert not ws.any(), "workspace must be left zeroed"
