@@ -268,7 +268,7 @@ def gemm_roofline(torch, eng, peaks, basis):
         for e, o, ol in zip(engines, origs, origs_ln):
             e._linear = o
             e._linear_ln = ol
-    ops_l, bytes_l = [], []
+    ops_l, bytes_l, fab_l = [], [], []
     for f, a in calls:
         q, w = a[0], a[2]
         m, k = q.shape
@@ -276,10 +276,13 @@ def gemm_roofline(torch, eng, peaks, basis):
         if len(a) == 5:
             out = a[4]
             nb = m * k + n * k * w.bits // 8 + m * n * out.element_size() + 4 * m + 8 * n
+            wr = m * n * out.element_size()
         else:  # GEMM + residual read + LN out f32 + int8 + scales
             nb = m * k + n * k + 4 * m * n + 4 * m * n + m * n + 8 * m + 16 * n
+            wr = 5 * m * n
         ops_l.append(2 * m * k * n)
         bytes_l.append(nb)
+        fab_l.append(fabric_time(m, n, k, wr, 2 * m * k * n, int8_peak(peaks)))
     st = torch.cuda.Stream()
     st.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(st):
@@ -316,7 +319,28 @@ def gemm_roofline(torch, eng, peaks, basis):
                            "HBM-bound and 4hh tensor-bound at BERT-base shapes; bytes dominate the sum",
             "tensor_tops": ops / t_per_pass / 1e12, "tensor_peak": p_int8 / 1e12,
             "frac_of_per_launch_roofline": t_roof / t_per_pass,
+            "fabric_roofline": {
+                "frac": sum(fab_l) / t_per_pass, "bound_us_per_launch": 1e6 * sum(fab_l) / n_l,
+                "basis": FABRIC_BASIS},
             "peak_basis": f"{basis} HBM copy bandwidth; " + INT8_PEAK_BASIS.format(basis=basis, **peaks)}
+
+
+# SM <-> L2 fabric of this B200, measured with tools/micro (profiles/r02/tma_read_bw.txt,
+# store_bw.txt): TMA reads alone 21 TB/s; SM -> L2 writes cap at 6.4 TB/s (all SMs);
+# with writes at that cap, reads get 9.7 TB/s, i.e. a written byte costs the shared
+# fabric as much as 21 / 11.9 read bytes.
+FABRIC_READ, FABRIC_WRITE_CAP, FABRIC_WRITE_COST = 21.0e12, 6.4e12, 11.9e12
+FABRIC_BASIS = ("per launch max(ops / P_int8, writes / 6.4 TB/s, operand reads / 21 TB/s + writes / 11.9 TB/s); "
+                "operand reads = A once per n-tile + B once per 256-row tile (the CTA-pair kernel's L2 -> SM "
+                "traffic), writes = the f32 outputs; fabric rates measured by tools/micro/tma_read_bw.cu and "
+                "store_bw.cu (profiles/r02/)")
+
+
+def fabric_time(m: int, n: int, k: int, wbytes: int, ops: int, p_int8: float, bn: int | None = None) -> float:
+    """Lower bound of one fused linear on the measured SM <-> L2 fabric (FABRIC_BASIS)."""
+    bn = bn or (256 if n % 256 == 0 or n > 2048 else 192)
+    reads = m * k * math.ceil(n / bn) + n * k * math.ceil(m / 256)
+    return max(ops / p_int8, wbytes / FABRIC_WRITE_CAP, reads / FABRIC_READ + wbytes / FABRIC_WRITE_COST)
 
 
 INT8_NOMINAL_TOPS = 4500.0

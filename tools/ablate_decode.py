@@ -12,7 +12,7 @@ from paper_2206_01861_b200 import _native as N  # noqa: E402
 from paper_2206_01861_b200 import decoder as D  # noqa: E402
 
 FAMILIES = {
-    "linear": ("zq_linear",),
+    "linear": ("zq_linear", "zq_linear_ws", "zq_linear_kv_ws"),
     "decode_attention": ("zq_decode_attention_f32",),
     "kv_append": ("zq_kv_append",),
     "ln": ("zq_layer_norm_quantize",),

@@ -30,7 +30,7 @@ def chain(fn, n=64):
     return a.elapsed_time(b) / n * 1e3
 
 
-for name, t, d, f in (("gpt3-350m", 8, 1024, 4096), ("gptj-6b", 16, 4096, 16384)):
+for name, t, d, f in (("gpt3-350m", 8, 1024, 4096), ("gptj-6b", 16, 4096, 16384), ("neox-20b", 16, 6144, 24576)):
     x = torch.randn(t, d, device="cuda")
     res = torch.randn(t, d, device="cuda")
     u = torch.randn(t, f, device="cuda")
