@@ -216,6 +216,16 @@ int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, cons
                  int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
                  float* out, int64_t ld_out, float* kcache, float* vcache, const int32_t* pos, int dmodel_local,
                  int64_t max_ctx, void* stream);
+/* Prefill QKV projection (M > 64 token rows = whole sequences of rows_per_seq
+ * tokens, the cache empty before it) with the KV-cache append done by the
+ * CTA-pair GEMM's epilogue: row r's k / v columns also go to cache row
+ * (r / rows_per_seq) * max_ctx + r % rows_per_seq.  ZQ_ERR_UNSUPPORTED where the
+ * pair path does not apply (the caller runs zq_linear + zq_kv_append). */
+int zq_linear_kv_prefill(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                         int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                         float* out, int64_t ld_out, float* kcache, float* vcache, int dmodel_local, int64_t max_ctx,
+                         int rows_per_seq, void* stream);
+
 /* The same with the stream-K workspace (see zq_linear_ws). */
 int zq_linear_kv_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
                     int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,

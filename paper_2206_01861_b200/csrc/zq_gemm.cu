@@ -333,7 +333,8 @@ struct Gemm2Cfg {
 template <int BN, int KIND, int CL>
 __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
     zq_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmKc,
+                    const __grid_constant__ CUtensorMap tmVc, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   // no static smem: the dynamic window is 1024-aligned (checked below), and using
@@ -528,6 +529,13 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0 && !(p.debug & 1)) {
             tma_store_2d(&tmC, sb, col0, row0);
+            if (p.kv_rows_per_seq > 0 && col0 >= p.kv_dl) {
+              // prefill: the k / v columns of these 32 token rows also go to the KV
+              // cache rows b * max_ctx + t (one sequence per 32-row box)
+              const int crow = (int)((int64_t)(row0 / p.kv_rows_per_seq) * p.kv_max_ctx + row0 % p.kv_rows_per_seq);
+              if (col0 < 2 * p.kv_dl) tma_store_2d(&tmKc, sb, col0 - p.kv_dl, crow);
+              else tma_store_2d(&tmVc, sb, col0 - 2 * p.kv_dl, crow);
+            }
             bulk_commit();
           }
           sbuf ^= 1;
@@ -1499,7 +1507,7 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 
 template <int BN, int KIND, int CL>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, GemmParams p,
-                          cudaStream_t st) {
+                          cudaStream_t st, const CUtensorMap* tkc = nullptr, const CUtensorMap* tvc = nullptr) {
   using Cfg = Gemm2Cfg<BN>;
   static ZqDeviceOnce attr_once;
   attr_once([&](int) {
@@ -1536,7 +1544,7 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   }
   const int clusters = units < max_clusters ? units : max_clusters;
   const cudaError_t e = launch_kernel(zq_gemm2_kernel<BN, KIND, CL>, dim3(CL * clusters), dim3(Cfg::NUM_THREADS),
-                                      Cfg::SMEM_BYTES, st, CL, ta, tb, tc, p);
+                                      Cfg::SMEM_BYTES, st, CL, ta, tb, tc, tkc ? *tkc : tc, tvc ? *tvc : tc, p);
   if (e != cudaSuccess) {
     set_error("tcgen05 cta-pair gemm launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
@@ -1873,6 +1881,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       if (bn2 && (force_cl == 2 || (force_cl == 4 && (N + bn2 - 1) / bn2 >= 2))) cl2 = force_cl;
     }
     if (bn2 && w_bits == 4) {
+      if (p.kv_rows_per_seq > 0) return ZQ_ERR_UNSUPPORTED;
       p.trace = g_trace;
       p.debug = g_debug;
       return gemm2c_w4i8(xq, ld_x, wq, ld_w, M, N, K, kind, bn2 == 192 ? 256 : bn2, p, st);
@@ -1912,9 +1921,25 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
       p.num_tiles = (int)mp * p.num_n_tiles;
       p.num_k_blocks = (int)((K + BLOCK_K - 1) / BLOCK_K);
       p.group_m = K >= 2048 ? 8 : 1;  // operand-bound: keep A / B panels in L2
-#define ZQ_G2C(KK, CC) (bn2 == 256 ? launch_gemm2_t<256, KK, CC>(ta, tb, tc, p, st) \
-                        : bn2 == 192 ? launch_gemm2_t<192, KK, CC>(ta, tb, tc, p, st)  \
-                                     : launch_gemm2_t<128, KK, CC>(ta, tb, tc, p, st))
+      CUtensorMap tkc, tvc;
+      const CUtensorMap* pkc = nullptr;
+      const CUtensorMap* pvc = nullptr;
+      if (p.kv_rows_per_seq > 0) {  // prefill KV append through the epilogue (f32 output only)
+        if (kind != OUT_F32 || !p.tma_out || p.kv_rows_per_seq % 32 != 0 || p.kv_dl % 32 != 0 ||
+            M % p.kv_rows_per_seq != 0)
+          return ZQ_ERR_UNSUPPORTED;
+        const int64_t crows = (M / p.kv_rows_per_seq) * p.kv_max_ctx;
+        int rk = make_tmap_2d(&tkc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.kc, crows, p.kv_dl, (int64_t)p.kv_dl * 4, 32,
+                              32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (!rk) rk = make_tmap_2d(&tvc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.vc, crows, p.kv_dl, (int64_t)p.kv_dl * 4,
+                                   32, 32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (rk) return rk;
+        pkc = &tkc;
+        pvc = &tvc;
+      }
+#define ZQ_G2C(KK, CC) (bn2 == 256 ? launch_gemm2_t<256, KK, CC>(ta, tb, tc, p, st, pkc, pvc) \
+                        : bn2 == 192 ? launch_gemm2_t<192, KK, CC>(ta, tb, tc, p, st, pkc, pvc)  \
+                                     : launch_gemm2_t<128, KK, CC>(ta, tb, tc, p, st, pkc, pvc))
 #define ZQ_G2(KK) (cl2 == 4 ? ZQ_G2C(KK, 4) : ZQ_G2C(KK, 2))
       switch (kind) {
         case OUT_S32: return ZQ_G2(OUT_S32);
@@ -1925,6 +1950,7 @@ static int gemm_common(const int8_t* xq, int64_t ld_x, const void* wq, int64_t l
 #undef ZQ_G2
     }
   }
+  if (p.kv_rows_per_seq > 0) return ZQ_ERR_UNSUPPORTED;  // prefill KV append: CTA-pair path only
   const int bn = pick_bn(M, N);
   CUtensorMap ta, tb;
   int rc = make_tmap_u8(&ta, xq, M, K, ld_x, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -2047,6 +2073,30 @@ int zq_linear_ws(const int8_t* xq, int64_t ld_x, const float* token_scales, floa
   p.sk_ws = reinterpret_cast<int32_t*>(workspace);
   p.sk_ws_bytes = workspace_bytes;
   return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, out_type + 1, p, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zq_linear_kv_prefill(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,
+                         int w_bits, const float* w_row_scales, const float* bias, int64_t M, int64_t N, int64_t K,
+                         float* out, int64_t ld_out, float* kcache, float* vcache, int dmodel_local, int64_t max_ctx,
+                         int rows_per_seq, void* stream) {
+  ZQ_CHECK_ARG(w_row_scales != nullptr && kcache && vcache, ZQ_ERR_USAGE, "linear + kv append needs every operand");
+  ZQ_CHECK_ARG(N == 3LL * dmodel_local && ld_out >= N, ZQ_ERR_SHAPE, "qkv output must be 3 x dmodel_local wide");
+  ZQ_CHECK_ARG(rows_per_seq >= 1 && rows_per_seq <= max_ctx && M % rows_per_seq == 0, ZQ_ERR_SHAPE,
+               "prefill rows must be whole sequences of <= max_ctx tokens");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.out = out;
+  p.ld_out = ld_out;
+  p.token_scales = token_scales;
+  p.row_scales = w_row_scales;
+  p.bias = bias;
+  p.kc = kcache;
+  p.vc = vcache;
+  p.kv_dl = dmodel_local;
+  p.kv_max_ctx = max_ctx;
+  p.kv_rows_per_seq = rows_per_seq;
+  if (M <= 64) return ZQ_ERR_UNSUPPORTED;
+  return gemm_common(xq, ld_x, wq, ld_w, w_bits, M, N, K, OUT_F32, p, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int zq_linear_kv(const int8_t* xq, int64_t ld_x, const float* token_scales, const void* wq, int64_t ld_w,

@@ -42,6 +42,9 @@ struct GemmParams {
   // partial sums, left zeroed by every launch (nullable)
   int32_t* sk_ws;
   int64_t sk_ws_bytes;
+  // prefill QKV (CTA-pair path, cache empty): output row r also goes to cache row
+  // (r / kv_rows_per_seq) * kv_max_ctx + r % kv_rows_per_seq (0 = off)
+  int kv_rows_per_seq;
 };
 
 __device__ __forceinline__ void bulk_wait_read1() {

@@ -191,6 +191,19 @@ class DecoderEngine:
                        self.dl, self.max_ctx, self._sk_ws.data_ptr(), 4 * self._sk_ws.numel(), N.stream_ptr())
         return rc != N.ZQ_ERR_UNSUPPORTED
 
+    def _qkv_kv_prefill(self, xq, sx, blk, qkv, li: int, t: int, rows_per_seq: int) -> bool:
+        """Prefill QKV linear with the KV-cache append in the CTA-pair GEMM epilogue
+        (prefill starts from an empty cache: pos = 0); False when unsupported."""
+        if os.environ.get("ZQ_KV_PREFILL", "1") == "0":
+            return False
+        w = blk.w_qkv
+        wp, ldw, wb = w.weight_operand()
+        rc = N.call_rc("zq_linear_kv_prefill", xq.data_ptr(), xq.stride(0), sx.data_ptr(), wp, ldw, wb,
+                       w.row_scales().data_ptr(), blk.b_qkv.data_ptr(), t, w.rows, xq.shape[1], qkv.data_ptr(),
+                       qkv.stride(0), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(), self.dl,
+                       self.max_ctx, rows_per_seq, N.stream_ptr())
+        return rc != N.ZQ_ERR_UNSUPPORTED
+
     def _tok_quant(self, x, q, s):
         t, d = x.shape
         N.call("zq_quantize_tokenwise", x.data_ptr(), t, d, x.stride(0), 8, q.data_ptr(), q.stride(0),
@@ -220,7 +233,13 @@ class DecoderEngine:
         x, xq, sx = B["x"], B["xq"], B["sx"]
         for li, blk in enumerate(self.blocks):
             qkv = B["qkv"]
-            if prefill or not self._qkv_kv(xq, sx, blk, qkv, li, t):
+            if prefill:
+                if not self._qkv_kv_prefill(xq, sx, blk, qkv, li, t, rows_per_seq):
+                    self._linear(xq, sx, blk.w_qkv, blk.b_qkv, qkv)
+                    N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), self.batch, rows_per_seq, dl,
+                           self.pos.data_ptr(), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(),
+                           self.max_ctx, N.stream_ptr())
+            elif not self._qkv_kv(xq, sx, blk, qkv, li, t):
                 self._linear(xq, sx, blk.w_qkv, blk.b_qkv, qkv)
                 N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), self.batch, rows_per_seq, dl,
                        self.pos.data_ptr(), self.kcache[li].data_ptr(), self.vcache[li].data_ptr(),

@@ -206,3 +206,45 @@ def test_flag_cleared_by_prefill():
     eng.flag.fill_(1)
     eng.prefill(np.zeros((2, 4), np.int64))
     eng.check_finite()
+
+
+@pytest.mark.parametrize("shape", [(8, 1024, 1024, 1040), (16, 128, 4096, 256), (8, 256, 768, 300),
+                                   (2, 256, 768, 300), (16, 100, 1024, 128)])
+def test_linear_kv_prefill_matches_linear_then_append(shape):
+    """zq_linear_kv_prefill (KV-cache append in the CTA-pair GEMM epilogue) ==
+    zq_linear + zq_kv_append: the qkv output and both caches bit for bit.  Shapes
+    off the pair path (few rows) or with sequences not a multiple of 32 tokens
+    return ZQ_ERR_UNSUPPORTED (the decoder then runs the unfused pair)."""
+    from paper_2206_01861_b200 import _native as N
+    from paper_2206_01861_b200 import quant
+
+    batch, T, dl, max_ctx = shape
+    m = batch * T
+    rng = np.random.default_rng(sum(shape))
+    xq = quant.quantize_activation_tokenwise(torch.from_numpy(rng.standard_normal((m, dl)).astype(np.float32)).cuda(), 8)
+    w = quant.quantize_weight_groupwise(torch.from_numpy((rng.standard_normal((3 * dl, dl)) * 0.02).astype(np.float32)).cuda(), 16, 8)
+    bias = torch.from_numpy((rng.standard_normal(3 * dl) * 0.1).astype(np.float32)).cuda()
+    a = xq.gemm_operand()
+    wp, ldw, wb = w.weight_operand()
+    outs = []
+    for fused in (False, True):
+        qkv = torch.empty(m, 3 * dl, device="cuda")
+        kc = torch.full((batch, max_ctx, dl), 7.0, device="cuda")
+        vc = torch.full((batch, max_ctx, dl), 7.0, device="cuda")
+        pos = torch.zeros(batch, dtype=torch.int32, device="cuda")
+        if fused:
+            rc = N.call_rc("zq_linear_kv_prefill", a.data_ptr(), a.stride(0), xq.token_scales.data_ptr(), wp, ldw,
+                           wb, w.row_scales().data_ptr(), bias.data_ptr(), m, 3 * dl, dl, qkv.data_ptr(),
+                           qkv.stride(0), kc.data_ptr(), vc.data_ptr(), dl, max_ctx, T, N.stream_ptr())
+            if rc == N.ZQ_ERR_UNSUPPORTED:
+                assert T % 32 != 0 or m // 256 * (3 * dl // 128) < 74, shape
+                return
+        else:
+            N.call("zq_linear", a.data_ptr(), a.stride(0), xq.token_scales.data_ptr(), 0.0, wp, ldw, wb,
+                   w.row_scales().data_ptr(), bias.data_ptr(), m, 3 * dl, dl, qkv.data_ptr(), qkv.stride(0),
+                   N.OUT_F32, N.stream_ptr())
+            N.call("zq_kv_append", qkv.data_ptr(), qkv.stride(0), batch, T, dl, pos.data_ptr(), kc.data_ptr(),
+                   vc.data_ptr(), max_ctx, N.stream_ptr())
+        outs.append((qkv, kc, vc))
+    for a0, a1 in zip(outs[0], outs[1]):
+        assert torch.equal(a0.view(torch.int32), a1.view(torch.int32)), shape
