@@ -797,6 +797,347 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Long sequences (seq > 128, head_dim 64: GPT-3 350M prefill) with the fp16
+// two-term scheme of attention_f16_kernel and an online softmax over 128-key
+// blocks.  Work items are (sequence, head, 128-query block), heaviest causal
+// blocks first; a CTA walks the key blocks of its items as one flat sequence of
+// steps with the same software pipeline (the split of step j+1 on the CUDA
+// cores runs while the tensor core computes P V of step j).  Q's hi / lo stay in
+// TMEM for all key blocks of an item; K and V get a power-of-two scale per
+// block (fk_j, fv_j), folded exactly into the softmax exponent (S) and into the
+// running O; P is split with a per-row, per-block power of two that puts the
+// block's largest p in [2^14, 2^15) (a block far below the running max keeps its
+// precision).  Before step j's P V, O is rescaled in TMEM by corr_j and the ratio
+// of the two blocks' P and V scales, so it always carries the current block's.
+// Replaces the 3xTF32 kernel (attention_long_kernel, kept under ZQ_ATT_LONG_TF32=1):
+// twice the MMA rate and half the operand bytes per term.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1)
+    attention_f16_long_kernel(const __grid_constant__ CUtensorMap tm, int seq, int heads, int dmodel, int causal,
+                              float scale, float* __restrict__ ctx, int64_t ld_ctx, int nbh, int nq) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + kRegion;
+  uint8_t* sV = sm + 2 * kRegion;
+  uint8_t* sKh = sm + 3 * kRegion;
+  uint8_t* sKl = sKh + kH16;
+  uint8_t* sVT = sKl + kH16;  // [2 buffers][hi | lo]
+  uint8_t* sO = sVT + 4 * kH16;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + kRegion);  // raw, -, S, O
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bar + 5);     // [8 warps][3]
+  float* red = reinterpret_cast<float*>(rmax + 24);          // [2][128] row partials
+  (void)sO;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    prefetch_tmap(&tm);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+  const int nitems = nbh * nq;
+
+  // item -> (b, h, qb), the heaviest causal query blocks first; nk key blocks
+  auto decode = [&](int item, int& b, int& h, int& qb) {
+    qb = nq - 1 - item / nbh;
+    const int bh = item % nbh;
+    b = bh / heads;
+    h = bh % heads;
+  };
+  auto nkeys = [&](int qb) { return causal ? qb + 1 : nq; };
+  // the step after (item, kb) for this CTA; item = nitems when there is none
+  auto next_step = [&](int item, int kb, int& nitem, int& nkb) {
+    int b, h, qb;
+    decode(item, b, h, qb);
+    if (kb + 1 < nkeys(qb)) {
+      nitem = item, nkb = kb + 1;
+    } else {
+      nitem = item + (int)gridDim.x, nkb = 0;
+    }
+  };
+  auto issue_raw = [&](int item, int kb) {
+    int b, h, qb;
+    decode(item, b, h, qb);
+    mbar_arrive_expect_tx(&bar[0], (kb == 0 ? 6 : 4) * 128 * 128);
+#pragma unroll
+    for (int part = 0; part < 3; ++part) {
+      if (part == 0 && kb != 0) continue;  // Q stays in TMEM for the item's later key blocks
+      const int r0 = b * seq + (part == 0 ? qb : kb) * kAttT;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        tma_load_2d(sm + part * kRegion + j * (kRegion / 2), &tm, &bar[0], part * dmodel + h * kAttD + 32 * j, r0);
+    }
+  };
+
+  // raw tiles of a step (landed) -> [Q hi/lo into TMEM when kb == 0], K hi/lo and
+  // V^T hi/lo (buffer vb) in smem, with their power-of-two scales; issues the raw
+  // loads of (aitem, akb) as soon as every thread has read the raw tiles
+  auto split = [&](bool with_q, int aitem, int akb, int vb, float& fq, float& fk, float& fv) {
+    float q[32], k[32], v[32];
+    {
+      const uint8_t* qr = sQ + half * (kRegion / 2) + row * 128;
+      const uint8_t* kr = sK + half * (kRegion / 2) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 bb = *reinterpret_cast<const float4*>(kr + ((c ^ (row & 7)) << 4));
+        k[4 * c] = bb.x, k[4 * c + 1] = bb.y, k[4 * c + 2] = bb.z, k[4 * c + 3] = bb.w;
+        if (with_q) {
+          const float4 a = *reinterpret_cast<const float4*>(qr + ((c ^ (row & 7)) << 4));
+          q[4 * c] = a.x, q[4 * c + 1] = a.y, q[4 * c + 2] = a.z, q[4 * c + 3] = a.w;
+        } else {
+          q[4 * c] = q[4 * c + 1] = q[4 * c + 2] = q[4 * c + 3] = 0.0f;
+        }
+      }
+    }
+    const int vd = tid & 63, vtb = tid >> 6;
+    {
+      const uint8_t* vc = sV + (vd >> 5) * (kRegion / 2) + (vd & 3) * 4;
+      const int jc = (vd & 31) >> 2;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int t = 32 * vtb + i;
+        v[i] = *reinterpret_cast<const float*>(vc + t * 128 + ((jc ^ (t & 7)) << 4));
+      }
+    }
+    uint32_t mq = 0, mk = 0, mv = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      mq = max(mq, __float_as_uint(q[i]) & 0x7fffffffu);
+      mk = max(mk, __float_as_uint(k[i]) & 0x7fffffffu);
+      mv = max(mv, __float_as_uint(v[i]) & 0x7fffffffu);
+    }
+    mq = __reduce_max_sync(0xffffffffu, mq);
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    mv = __reduce_max_sync(0xffffffffu, mv);
+    __syncthreads();
+    if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
+    __syncthreads();
+    if (tid == 0 && aitem < nitems) issue_raw(aitem, akb);
+    {
+      const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
+                     cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+      mq = __reduce_max_sync(0xffffffffu, a);
+      mk = __reduce_max_sync(0xffffffffu, bq);
+      mv = __reduce_max_sync(0xffffffffu, cq);
+    }
+    fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
+    if (with_q) {
+      fq = pow2_scale_for(mq);
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 16 * half, hi);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 32 + 16 * half, lo);
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = row * 128 + ((((4 * half + c) ^ (row & 7))) << 4);
+        *reinterpret_cast<uint4*>(sKh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sKl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(v[2 * j], fv), __fmul_rn(v[2 * j + 1], fv), hi[j], lo[j]);
+      uint8_t* vh = sVT + vb * (2 * kH16);
+      uint8_t* vl = vh + kH16;
+      const uint32_t atom = (uint32_t)(vtb >> 1) * (64 * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = atom + vd * 128 + ((((4 * (vtb & 1) + c) ^ (vd & 7))) << 4);
+        *reinterpret_cast<uint4*>(vh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(vl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    tmem_st_wait();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto issue_s = [&]() {
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, 128);
+      const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttD / 16; ++ks)
+          mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks, idesc,
+                           (t3 | ks) != 0);
+      mma_commit_elect(&bar[2]);
+    }
+  };
+
+  pdl_trigger();
+  pdl_wait();
+  float fq = 1.0f, fk = 1.0f, fv = 1.0f;
+  int item = blockIdx.x, kb = 0;
+  if (item < nitems) {
+    if (tid == 0) issue_raw(item, 0);
+    mbar_wait(&bar[0], 0);
+    int ni, nk2;
+    next_step(item, 0, ni, nk2);
+    split(true, ni, nk2, 0, fq, fk, fv);
+    issue_s();
+  }
+  float m2 = -INFINITY, l = 0.0f, fv_prev = 1.0f;
+  int kp_prev = 0;
+  for (int it = 0; item < nitems; ++it) {
+    const uint32_t ph = it & 1;
+    int b, h, qb;
+    decode(item, b, h, qb);
+    const int nk = nkeys(qb);
+    const int q0 = qb * kAttT;
+    int nitem, nkb;
+    next_step(item, kb, nitem, nkb);
+    const float cfq = fq, cfk = fk, cfv = fv;  // this step's scales (split of the next overwrites)
+    mbar_wait(&bar[2], ph);
+    tc_fence_after();
+
+    // ---- online softmax of this key block ----
+    float s[64];
+    {
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem + lane_base + half * 64;
+      tmem_ld_32x32b_x32(ta, r0);
+      tmem_ld_32x32b_x32(ta + 32, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        s[j] = __uint_as_float(r0[j]);
+        s[32 + j] = __uint_as_float(r1[j]);
+      }
+    }
+    float mx = -INFINITY;
+    const int k0 = kb * kAttT + half * 64;
+    if ((causal && kb == qb) || k0 + 64 > seq) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = k0 + j;
+        if (key >= seq || (causal && key > q0 + row)) s[j] = -INFINITY;  // transformer.py:433-434
+        mx = fmaxf(mx, s[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
+    }
+    red[half * 128 + row] = mx;
+    __syncthreads();
+    mx = fmaxf(red[row], red[128 + row]);
+    // scores in log2 units: S' * c with c = scale log2(e) / (fq fk_j) (exact powers of two)
+    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
+    const float mxb = __fmul_rn(mx, c);
+    const float m2_new = fmaxf(m2, mxb);
+    const float corr = ex2_approx_f(__fsub_rn(m2, m2_new));  // 0 on the first block (m2 = -inf)
+    // P' = p * 2^(14 - kp): the row's largest p of this block (2^(mxb - m2_new)) lands
+    // in [2^14, 2^15), so blocks far below the running max keep 22 significant bits
+    const int kp = max((int)floorf(__fsub_rn(mxb, m2_new)), -100);
+    const float mxc = __fsub_rn(m2_new, (float)(14 - kp));
+    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
+      s[j] = e;
+      sp[j & 3] = __fadd_rn(sp[j & 3], e);
+    }
+    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+    __syncthreads();
+    red[half * 128 + row] = sum;
+    __syncthreads();
+    sum = __fmul_rn(__fadd_rn(red[row], red[128 + row]), ldexpf(1.0f, kp - 14));  // true units
+    l = kb == 0 ? sum : __fadd_rn(__fmul_rn(l, corr), sum);
+    m2 = m2_new;
+    {
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) split_f16x2(s[2 * j], s[2 * j + 1], hi[j], lo[j]);
+      tmem_st_32x32b_x32u(tmem + lane_base + 32 * half, hi);
+      tmem_st_32x32b_x32u(tmem + lane_base + 64 + 32 * half, lo);
+    }
+    if (kb > 0) {  // O carries 2^(14-kp) fv of the previous block: rescale by corr * 2^(kp' - kp) fv_j / fv_{j-1}
+      const float f = __fmul_rn(__fmul_rn(__fmul_rn(corr, cfv), pow2_inv(fv_prev)), ldexpf(1.0f, kp_prev - kp));
+      uint32_t r0[32];
+      const uint32_t ta = tmem + lane_base + kT16O + half * 32;
+      tmem_ld_32x32b_x32(ta, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), f));
+      tmem_st_32x32b_x32u(ta, r0);
+    }
+    fv_prev = cfv;
+    kp_prev = kp;
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // ---- O' += P' V' (3 terms), A = P' from TMEM, B = V'^T buffer it & 1 ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, kAttD);
+      const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
+      const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttT / 16; ++ks) {
+          const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
+          mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                           (kb | t3 | ks) != 0);
+        }
+      mma_commit_elect(&bar[3]);
+    }
+    // ---- the next step's split runs while the tensor core computes P V ----
+    if (nitem < nitems) {
+      mbar_wait(&bar[0], (it + 1) & 1);
+      int ai, akb;
+      next_step(nitem, nkb, ai, akb);
+      split(nkb == 0, ai, akb, (it + 1) & 1, fq, fk, fv);
+    }
+    mbar_wait(&bar[3], ph);
+    tc_fence_after();
+    if (nitem < nitems) issue_s();  // P of this step is consumed: S of the next may overwrite it
+    if (kb == nk - 1) {
+      // ---- the item's output: O' / (l * 2^(14 - kp) * fv_last) ----
+      const float oscale = __fmul_rn(__fmul_rn(__frcp_rn(l), pow2_inv(cfv)), ldexpf(1.0f, kp - 14));
+      uint32_t r0[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
+      tmem_ld_wait();
+      if (q0 + row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + q0 + row) * ld_ctx + h * kAttD + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(
+              __fmul_rn(__uint_as_float(r0[j]), oscale), __fmul_rn(__uint_as_float(r0[j + 1]), oscale),
+              __fmul_rn(__uint_as_float(r0[j + 2]), oscale), __fmul_rn(__uint_as_float(r0[j + 3]), oscale));
+      }
+      m2 = -INFINITY;
+      l = 0.0f;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    item = nitem;
+    kb = nkb;
+  }
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+// ---------------------------------------------------------------------------
 // Any head_dim (multiple of 32, <= 256) and any sequence length: CUDA-core fp32
 // flash attention (GPT-J 256 / NeoX 96 prefill).  A CTA takes 32 queries of one
 // (sequence, head): 4 warps x 8 query rows; per block of 32 keys lane l scores key
@@ -1276,6 +1617,7 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem);
     cudaFuncSetAttribute(attention_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAtt16Smem);
+    cudaFuncSetAttribute(attention_f16_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAtt16Smem);
   });
   const int nsm = zq_num_sms();
   const int total = batch * heads;
@@ -1307,9 +1649,19 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
     const int nq = (seq + kAttT - 1) / kAttT;
     const int items = total * nq;
     const int grid = items < nsm ? items : nsm;
-    e = launch_kernel(attention_long_kernel, dim3(grid), dim3(256), kAttSmem,
-                      reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads, heads * head_dim, causal,
-                      scale, ctx, ld_ctx, total, nq);
+    static int long_tf32 = -1;  // ZQ_ATT_LONG_TF32=1: the 3xTF32 long-sequence kernel
+    if (long_tf32 < 0) {
+      const char* ev = getenv("ZQ_ATT_LONG_TF32");
+      long_tf32 = ev ? atoi(ev) : 0;
+    }
+    if (long_tf32)
+      e = launch_kernel(attention_long_kernel, dim3(grid), dim3(256), kAttSmem,
+                        reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads, heads * head_dim, causal,
+                        scale, ctx, ld_ctx, total, nq);
+    else
+      e = launch_kernel(attention_f16_long_kernel, dim3(grid), dim3(256), kAtt16Smem,
+                        reinterpret_cast<cudaStream_t>(stream), 1, tm, seq, heads, heads * head_dim, causal,
+                        scale, ctx, ld_ctx, total, nq);
   }
   if (e != cudaSuccess) {
     set_error("attention launch: %s", cudaGetErrorString(e));

@@ -65,3 +65,32 @@ def test_attention_separate_qkv_tensors_are_packed():
     out = T.attention(q, k, v, 4, False, 2)
     ref = ref_attention(torch.cat([q, k, v], 1), 2, 32, 4, 64, False)
     assert ((out.double() - ref).norm() / ref.norm()).item() < 1e-5
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_long_attention_per_block_scales(causal):
+    """seq > 128 runs the fp16 two-term online-softmax kernel with one power-of-two
+    scale per 128-key block for K and V: key blocks of very different magnitudes
+    (x1e-3 .. x1e3) must keep the ~fp32 accuracy (the running O is rescaled by
+    fv_j / fv_{j-1} between blocks)."""
+    from paper_2206_01861_b200 import transformer as T
+
+    batch, heads, dh, seq = 2, 4, 64, 640
+    d = heads * dh
+    torch.manual_seed(7 + causal)
+    qkv = torch.randn(batch * seq, 3 * d, device="cuda")
+    mags = torch.tensor([1e-3, 1.0, 1e3, 0.05, 20.0], device="cuda")
+    for bi in range(batch):
+        for kb in range(5):
+            rows = slice(bi * seq + kb * 128, bi * seq + (kb + 1) * 128)
+            qkv[rows, d:2 * d] *= mags[kb] ** 0.5 * 0.05   # keys: moderate logits
+            qkv[rows, 2 * d:] *= mags[(kb + 2) % 5]        # values: widely varying blocks
+    out = T.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], heads, causal, batch)
+    ref = ref_attention(qkv, batch, seq, heads, dh, causal)
+    # per (token, head) output row, relative to that row's own magnitude (outputs
+    # span ~6 orders of magnitude here); float32 attention itself is good to ~1e-5
+    diff = (out.double() - ref).view(batch * seq, heads, dh).abs().amax(-1)
+    scale = ref.view(batch * seq, heads, dh).abs().amax(-1)
+    err = (diff / scale).max().item()
+    rel = ((out.double() - ref).norm() / ref.norm()).item()
+    assert rel < 3e-5 and err < 1e-4, (rel, err)
