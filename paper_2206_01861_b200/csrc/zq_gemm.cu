@@ -1690,9 +1690,7 @@ static int launch_streamk_t(const CUtensorMap& tw, const CUtensorMap& tx, const 
   });
   cudaError_t e = launch_kernel(zq_gemm_streamk_kernel<MP, KIND>, dim3(grid), dim3(192), Cfg::SMEM_BYTES, st, 1, tw,
                                 tx, p);
-  static int noepi = -1;  // diagnostics: ZQ_SK_NOEPI=1 skips the epilogue kernel (wrong results)
-  if (noepi < 0) noepi = getenv("ZQ_SK_NOEPI") ? 1 : 0;
-  if (e == cudaSuccess && !noepi) {
+  if (e == cudaSuccess) {
     const int64_t total = (int64_t)p.M * (p.N / 4);
     const int eg = (int)std::min<int64_t>((total + 255) / 256, (int64_t)zq_num_sms() * 8);
     e = launch_kernel(skinny_sum_epilogue_kernel<KIND>, dim3(eg), dim3(256), 0, st, 1, p.sk_ws, MP, p);
