@@ -13,6 +13,8 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "zq_common.cuh"
 #include "zq_gelu.cuh"
 #include "zq_rowops.h"
@@ -251,17 +253,45 @@ __global__ void pack_int4_kernel(const int8_t* __restrict__ q, int64_t rows, int
 }
 
 // TP: quantize with a given (all-reduced) per-row absmax.
-__global__ void quant_with_absmax_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
-                                         int64_t ld_x, const float* __restrict__ amax, int qm,
-                                         int8_t* __restrict__ q, int64_t ld_q,
-                                         float* __restrict__ scales) {
-  const int64_t total = rows * ld_q;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / ld_q, c = i - r * ld_q;
-    float s = scale_from_absmax(amax[r], qm);
-    if (c == 0) scales[r] = s;
-    q[i] = (c < cols) ? (int8_t)quantize_exact(x[r * ld_x + c], s, qm) : (int8_t)0;
+// Token-wise quantization with the all-reduced row max (tensor-parallel row-parallel
+// projections): one CTA per row (grid-stride), the scale and its reciprocal once per
+// row, float4 loads, the branch-free fast rounding with the exact fallback for
+// near-ties (the same arithmetic as tok_quant_kernel, so bit-identical to it).
+__global__ void __launch_bounds__(256) quant_with_absmax_kernel(const float* __restrict__ x, int64_t rows,
+                                                                int64_t cols, int64_t ld_x,
+                                                                const float* __restrict__ amax, int qm,
+                                                                int8_t* __restrict__ q, int64_t ld_q,
+                                                                float* __restrict__ scales) {
+  pdl_trigger();
+  pdl_wait();
+  const bool vec = (cols & 3) == 0 && (ld_x & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(q) & 3) == 0 && (ld_q & 3) == 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float s = scale_from_absmax(amax[r], qm);
+    const float inv = safe_rcp(s);
+    if (threadIdx.x == 0) scales[r] = s;
+    const float* xr = x + r * ld_x;
+    int8_t* qr = q + r * ld_q;
+    if (vec) {
+      const int64_t n4 = cols >> 2;
+      for (int64_t c = threadIdx.x; c < n4; c += blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(xr) + c);
+        bool amb = inv == 0.0f;
+        int o0 = qbf(v.x, inv, qm, kQMargin, amb), o1 = qbf(v.y, inv, qm, kQMargin, amb),
+            o2 = qbf(v.z, inv, qm, kQMargin, amb), o3 = qbf(v.w, inv, qm, kQMargin, amb);
+        if (amb) {
+          o0 = quantize_exact_slow(v.x, s, qm);
+          o1 = quantize_exact_slow(v.y, s, qm);
+          o2 = quantize_exact_slow(v.z, s, qm);
+          o3 = quantize_exact_slow(v.w, s, qm);
+        }
+        reinterpret_cast<uint32_t*>(qr)[c] = pack4(o0, o1, o2, o3);
+      }
+      for (int64_t c = cols + threadIdx.x; c < ld_q; c += blockDim.x) qr[c] = 0;
+    } else {
+      for (int64_t c = threadIdx.x; c < ld_q; c += blockDim.x)
+        qr[c] = c < cols ? (int8_t)quantize_exact(xr[c], s, qm) : (int8_t)0;
+    }
   }
 }
 
@@ -639,13 +669,13 @@ int zq_quantize_with_absmax(const float* x, int64_t rows, int64_t cols, int64_t 
   ZQ_CHECK_ARG(bits_ok(bits), ZQ_ERR_USAGE, "unsupported bit width %d", bits);
   ZQ_CHECK_ARG(rows >= 1 && cols >= 1 && ld_x >= cols && ld_q >= cols && ld_q % 16 == 0,
                ZQ_ERR_USAGE, "bad shape");
-  int64_t total = rows * ld_q;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  quant_with_absmax_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, rows, cols, ld_x, amax,
-                                                                  qmax_of(bits), q, ld_q,
-                                                                  token_scales);
-  ZQ_LAUNCH_CHECK("quantize with absmax launch");
+  const int blocks = (int)std::min<int64_t>(rows, (int64_t)zq_num_sms() * 8);
+  const cudaError_t e = launch_kernel(quant_with_absmax_kernel, dim3(blocks), dim3(256), 0, as_stream(stream), 1, x,
+                                      rows, cols, ld_x, amax, qmax_of(bits), q, ld_q, token_scales);
+  if (e != cudaSuccess) {
+    set_error("quantize with absmax launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
   return ZQ_OK;
 }
 

@@ -335,3 +335,34 @@ def test_float64_inputs_follow_the_reference(zq):
         quant.quantize_array(np.array([1.0, np.inf]), 0.1, 8)
     with pytest.raises(ValueError):
         quant.compute_scale(np.array([np.nan]), 8)
+
+
+@pytest.mark.parametrize("shape", [(16, 6144), (2048, 768), (33, 1000), (5, 3), (7, 4096)])
+def test_quantize_with_absmax_matches_tokenwise(shape):
+    """zq_quantize_with_absmax (the TP row-parallel quantizer, given the all-reduced
+    row max) == the token-wise quantizer when given the local max, and == the
+    oracle's RHAFZ with the scale of a larger (other-rank) max; planted ties."""
+    from paper_2206_01861_b200 import _native as N
+    from paper_2206_01861_b200 import quant
+
+    rows, cols = shape
+    rng = np.random.default_rng(rows * 7 + cols)
+    x = rng.standard_normal((rows, cols)).astype(np.float32)
+    x[:, 0] = 127.0 / 2 * np.float32(0.03)  # candidates for exact half-way cases
+    xt = torch.from_numpy(x).cuda()
+    ld = (cols + 15) // 16 * 16
+    amax = torch.from_numpy(np.abs(x).max(axis=1).astype(np.float32)).cuda()
+    for mult in (1.0, 1.7):
+        am = amax * mult
+        q = torch.empty(rows, ld, dtype=torch.int8, device="cuda")
+        s = torch.empty(rows, device="cuda")
+        N.call("zq_quantize_with_absmax", xt.data_ptr(), rows, cols, cols, am.data_ptr(), 8, q.data_ptr(), ld,
+               s.data_ptr(), N.stream_ptr())
+        sref = np.array([np.float32(np.float64(v) / 127.0) for v in am.cpu().numpy()], dtype=np.float32)
+        assert np.array_equal(s.cpu().numpy().view(np.uint32), sref.view(np.uint32)), (shape, mult)
+        qref = np.stack([O.quantize_array(x[i], float(sref[i]), 8) for i in range(rows)])
+        assert np.array_equal(q[:, :cols].cpu().numpy(), qref), (shape, mult)
+        assert not q[:, cols:].any()
+        if mult == 1.0:
+            qa = quant.quantize_activation_tokenwise(xt, 8)
+            assert torch.equal(qa.values, q[:, :cols]) and torch.equal(qa.token_scales, s)
