@@ -134,6 +134,11 @@ int zq_linear_ln_quantize(const int8_t* xq, int64_t ld_x, const float* token_sca
                           float eps, int bits, float* ln_out, int8_t* q, int64_t ld_q, float* q_scales,
                           void* workspace, int64_t workspace_bytes, int32_t* nonfinite_flag, void* stream);
 
+/* zq_igemm_s32 with the stream-K workspace of zq_linear_ws for decode-sized calls
+ * (the tensor-parallel row-parallel partial GEMM before the int32 SUM all-reduce). */
+int zq_igemm_s32_ws(const int8_t* xq, int64_t ld_x, const void* wq, int64_t ld_w, int w_bits, int64_t M, int64_t N,
+                    int64_t K, int32_t* acc, int64_t ld_acc, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Standalone dequant epilogue over an int32 accumulator (igemm.py:83-112); used
  * after the tensor-parallel int32 all-reduce. */
 int zq_dequant_epilogue(const int32_t* acc, int64_t ld_acc, const float* token_scales,

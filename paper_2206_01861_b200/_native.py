@@ -66,6 +66,7 @@ _SIGS = {
                         _p, _i64, _p],
     "zq_linear_kv_prefill": [_p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _i32, _i64,
                              _i32, _p],
+    "zq_igemm_s32_ws": [_p, _i64, _p, _i64, _i32, _i64, _i64, _i64, _p, _i64, _p, _i64, _p],
     "zq_act_split16": [_p, _i64, _i64, _i64, _i32, _p, _p, _i64, _p, _p, _p],
     "zq_linear_wo": [_p, _p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p],
 }

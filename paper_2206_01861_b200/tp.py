@@ -207,6 +207,15 @@ class CudaOps:
         t = xq.values.shape[0]
         acc = self._buf(("acc", t, w.rows), lambda: torch.empty((t, w.rows), dtype=torch.int32,
                                                                 device=xq.values.device))
+        if t <= 64 and w.bits == 8:  # decode: the stream-K kernel, one reused zeroed workspace
+            nb = int(self.N.load().zq_linear_ws_bytes(t, w.rows))
+            ws = self._buf(("skws", t, w.rows), lambda: torch.zeros(nb // 4 + 4, dtype=torch.int32,
+                                                                    device=xq.values.device))
+            a = xq.gemm_operand()
+            wp, ldw, wb = w.weight_operand()
+            self.N.call("zq_igemm_s32_ws", a.data_ptr(), a.stride(0), wp, ldw, wb, t, w.rows, a.shape[1],
+                        acc.data_ptr(), acc.stride(0), ws.data_ptr(), 4 * ws.numel(), self.N.stream_ptr())
+            return acc
         return self.igemm.igemm(xq, w, out=acc).acc
 
     def epilogue(self, acc, scales, w, bias, out=None):
