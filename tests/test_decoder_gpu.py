@@ -248,3 +248,30 @@ def test_linear_kv_prefill_matches_linear_then_append(shape):
         outs.append((qkv, kc, vc))
     for a0, a1 in zip(outs[0], outs[1]):
         assert torch.equal(a0.view(torch.int32), a1.view(torch.int32)), shape
+
+
+@pytest.mark.parametrize("cfg_name", ["gpt3-350m", "gptj-6b"])
+def test_fused_prefill_kv_append_engine_bit_identical(cfg_name, monkeypatch):
+    """DecoderEngine prefill with the KV-cache append in the CTA-pair QKV GEMM's
+    epilogue (whole 32-token sequences, M large enough for the pair path) gives
+    the same caches, hidden state and greedy tokens, bit for bit, as the
+    separate zq_kv_append pass (ZQ_KV_PREFILL=0)."""
+    from paper_2206_01861_b200.decoder import CONFIGS, DecoderEngine
+
+    cfg = CONFIGS[cfg_name]
+    batch, T = (8, 256) if cfg_name == "gpt3-350m" else (16, 128)
+    ids = torch.from_numpy(np.random.default_rng(3).integers(0, cfg.vocab, (batch, T))).cuda()
+    res = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("ZQ_KV_PREFILL", env)
+        eng = DecoderEngine(cfg, batch, T + 4, seed=5, layers=2, use_graph=False)
+        toks = [eng.prefill(ids).clone()]
+        for _ in range(2):
+            toks.append(eng.step().clone())
+        res.append((torch.stack(toks, 1), eng.kcache[1][:, :T + 2].clone(), eng.vcache[0][:, :T + 2].clone(),
+                    eng._buffers(batch)["x"].clone()))
+        del eng
+        torch.cuda.empty_cache()
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a,
+                           b.view(torch.int32) if b.dtype == torch.float32 else b), cfg_name
