@@ -191,6 +191,21 @@ int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int seq, int h
                      int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
                      void* stream);
 
+/* Fused W8A8 QKV projection + attention for the encoder block (reference:
+ * pkg/src/lowbit/transformer.py:395-440 — quantized_linear(attn_in) on the
+ * concatenated QKV weight, then attention — which the reference runs as two
+ * steps).  xq [batch*seq, ld_x] int8 with token_scales [batch*seq] (dynamic
+ * token-wise), w_qkv [3*d, ld_w] int8 with w_row_scales [3*d] (expanded group
+ * scales) and bias [3*d] or NULL, d = heads*head_dim.  ctx is bit-identical to
+ * zq_linear(..., ZQ_OUT_F32) followed by zq_attention_f32; the f32 QKV
+ * activation never reaches HBM.  ZQ_ERR_UNSUPPORTED unless head_dim == 64,
+ * seq <= 128, d % 128 == 0 and ld_x, ld_w multiples of 16 (callers then run
+ * the two kernels). */
+int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* token_scales, const int8_t* w_qkv,
+                     int64_t ld_w, const float* w_row_scales, const float* bias, int batch, int seq,
+                     int heads, int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
+                     void* stream);
+
 /* GPT decode: scatter the k and v column blocks of the
  * fused QKV output qkv [batch*rows_per_seq, ld_qkv] (q | k | v, dmodel_local
  * columns each) into f32 caches [batch, max_ctx, dmodel_local] at rows

@@ -69,6 +69,7 @@ _SIGS = {
     "zq_igemm_s32_ws": [_p, _i64, _p, _i64, _i32, _i64, _i64, _i64, _p, _i64, _p, _i64, _p],
     "zq_act_split16": [_p, _i64, _i64, _i64, _i32, _p, _p, _i64, _p, _p, _p],
     "zq_linear_wo": [_p, _p, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _i64, _p, _i64, _i32, _p],
+    "zq_qkv_attention": [_p, _i64, _p, _p, _i64, _p, _p, _i32, _i32, _i32, _i32, _i32, _f32, _p, _i64, _p],
 }
 
 _lock = threading.Lock()

@@ -1555,8 +1555,403 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Fused QKV projection + attention (encoder, seq <= 128, head_dim 64).
+// One CTA per (sequence, head) unit computes that unit's 128 x 192 slice of the
+// W8A8 QKV linear (tokens b*seq.., weight rows {Q, K, V} x [64h, 64h+64)) with
+// tcgen05 kind::i8 into TMEM, dequantizes it exactly as the GEMM epilogue does
+// (((f32(acc) * s_tok) * s_w) + b, pkg/src/lowbit/igemm.py:131-139 — the values
+// zq_linear writes), and lays it out as the raw f32 Q | K | V tiles that
+// attention_f16_kernel loads by TMA; the attention then runs as in that kernel.
+// The [T, 3d] f32 QKV activation never leaves the SM: ctx is bit-identical to
+// zq_linear + zq_attention_f32 (tests/test_qkv_attention_gpu.py).
+//   warps 0-7: attention (attention_f16_kernel's code) + the GEMM epilogue
+//   warp 8   : TMA producer of the GEMM operands (3-stage ring over the raw region)
+//   warp 9   : GEMM MMA issuer
+//   smem: X = ring (3 x [A 128 x 128 B | B 192 x 128 B], 120 KB) or raw Q | K | V
+//         (f32, 96 KB) | K hi | K lo | 2 x (V^T hi | V^T lo) | barriers
+//   TMEM (512 cols): attention's [0, 256) + the GEMM accumulator [256, 448)
+// Pipeline: the GEMM of unit u+1 streams while the attention of unit u runs; the
+// ring is handed back to it by split(u) (barrier xfree).
+// ---------------------------------------------------------------------------
+constexpr int kQaStages = 3;
+constexpr int kQaStageA = 128 * 128, kQaStageB = 3 * kAttD * 128;
+constexpr int kQaStage = kQaStageA + kQaStageB;  // 40 KB
+constexpr int kQaX = kQaStages * kQaStage;       // 120 KB >= raw Q | K | V (96 KB)
+constexpr int kQaSmem = kQaX + 6 * kH16 + 128 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr uint32_t kQaAcc = 256;
+static_assert(kQaX >= 3 * kRegion, "raw tiles must fit the operand ring");
+
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(320, 1)
+    qkv_attention_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                         const float* __restrict__ ts, const float* __restrict__ rs, const float* __restrict__ bias,
+                         int M, int seq, int heads, int dmodel, int causal, float scale, float* __restrict__ ctx,
+                         int64_t ld_ctx, int nheads_total) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sX = sm;
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + kRegion;
+  uint8_t* sV = sm + 2 * kRegion;
+  uint8_t* sKh = sm + kQaX;
+  uint8_t* sKl = sKh + kH16;
+  uint8_t* sVT = sKl + kH16;  // [2 buffers][hi | lo]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVT + 4 * kH16);
+  uint64_t* gfull = bars;       // [3] operand stage landed
+  uint64_t* gempty = bars + 3;  // [3] operand stage consumed by the MMAs
+  uint64_t* accf = bars + 6;    // GEMM accumulator complete
+  uint64_t* xfree = bars + 7;   // raw tiles read (ring and accumulator free)
+  uint64_t* barS = bars + 8;
+  uint64_t* barO = bars + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 16);  // [8 warps][3]
+  float* red = reinterpret_cast<float*>(rmax + 24);         // [2][128] row partials
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkb = dmodel / 128;
+  if (tid == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 8) {  // ===== GEMM operand producer =====
+    if (lane == 0) {
+      int kc = 0, u = 0;
+      for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
+        if (u > 0) mbar_wait(xfree, (u - 1) & 1);
+        const int b = hd / heads, h = hd % heads;
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const int s = kc % kQaStages;
+          if (kc >= kQaStages) mbar_wait(&gempty[s], ((kc / kQaStages) - 1) & 1);
+          uint8_t* st = sX + s * kQaStage;
+          mbar_arrive_expect_tx(&gfull[s], kQaStage);
+          tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
+#pragma unroll
+          for (int part = 0; part < 3; ++part)
+            tma_load_2d(st + kQaStageA + part * (kAttD * 128), &tmW, &gfull[s], kb * 128,
+                        part * dmodel + h * kAttD);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 9) {  // ===== GEMM MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_i8(128, 3 * kAttD);
+      int kc = 0, u = 0;
+      for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
+        if (u > 0) mbar_wait(xfree, (u - 1) & 1);  // the epilogue has read the accumulator
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const int s = kc % kQaStages;
+          mbar_wait(&gfull[s], (kc / kQaStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sX + s * kQaStage);
+          const uint32_t b_addr = a_addr + kQaStageA;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_i8(tmem + kQaAcc, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32), idesc,
+                   (kb | k) != 0);
+          mma_commit(&gempty[s]);
+        }
+        mma_commit(accf);
+      }
+    }
+    return;
+  }
+
+  // ===== warps 0-7: GEMM epilogue + attention =====
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+
+  // accumulator of unit (hd, u) -> raw f32 Q | K | V tiles in the SW128 layout of
+  // attention_f16_kernel's TMA boxes (tile part, box j = columns [32j, 32j+32)).
+  // Rows past the last token are zero, as the TMA fill of the unfused path.
+  auto epilogue = [&](int hd, int u) {
+    const int b = hd / heads, h = hd % heads;
+    const int grow = b * seq + row;
+    const bool live = grow < M;
+    const float s_tok = live ? __ldg(ts + grow) : 0.0f;
+    mbar_wait(accf, u & 1);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c3 = 0; c3 < 3; ++c3) {
+      const int cc = half * 3 + c3;  // 32-column chunk of the 192
+      const int part = cc >> 1, box = cc & 1;
+      const int n0 = part * dmodel + h * kAttD + 32 * box;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + cc * 32, r);
+      tmem_ld_wait();
+      float f[32];
+      const float4* sw4 = reinterpret_cast<const float4*>(rs + n0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 w = __ldg(sw4 + j);
+        f[4 * j + 0] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x);
+        f[4 * j + 1] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y);
+        f[4 * j + 2] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z);
+        f[4 * j + 3] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w);
+      }
+      if (bias != nullptr) {
+        const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 bb = __ldg(b4 + j);
+          f[4 * j + 0] = __fadd_rn(f[4 * j + 0], bb.x);
+          f[4 * j + 1] = __fadd_rn(f[4 * j + 1], bb.y);
+          f[4 * j + 2] = __fadd_rn(f[4 * j + 2], bb.z);
+          f[4 * j + 3] = __fadd_rn(f[4 * j + 3], bb.w);
+        }
+      }
+      uint8_t* dst = sX + part * kRegion + box * (kRegion / 2) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<float4*>(dst + ((c ^ (row & 7)) << 4)) =
+            live ? make_float4(f[4 * c], f[4 * c + 1], f[4 * c + 2], f[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    tc_fence_before();
+    compute_bar();  // raw tiles complete
+  };
+
+
+  // raw tiles (written by epilogue) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo
+  // (buffer vb) in smem; returns the unit's three power-of-two scales and hands
+  // the raw region back to the GEMM (xfree).  As attention_f16_kernel's split.
+  auto split = [&](int vb, float& fq, float& fk, float& fv) {
+    float q[32], k[32], v[32];
+    {
+      const uint8_t* qr = sQ + half * (kRegion / 2) + row * 128;
+      const uint8_t* kr = sK + half * (kRegion / 2) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 a = *reinterpret_cast<const float4*>(qr + ((c ^ (row & 7)) << 4));
+        const float4 bb = *reinterpret_cast<const float4*>(kr + ((c ^ (row & 7)) << 4));
+        q[4 * c] = a.x, q[4 * c + 1] = a.y, q[4 * c + 2] = a.z, q[4 * c + 3] = a.w;
+        k[4 * c] = bb.x, k[4 * c + 1] = bb.y, k[4 * c + 2] = bb.z, k[4 * c + 3] = bb.w;
+      }
+    }
+    const int vd = tid & 63, vtb = tid >> 6;  // V^T row (head dim) and 32-token block
+    {
+      const uint8_t* vc = sV + (vd >> 5) * (kRegion / 2) + (vd & 3) * 4;
+      const int jc = (vd & 31) >> 2;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int t = 32 * vtb + i;
+        v[i] = *reinterpret_cast<const float*>(vc + t * 128 + ((jc ^ (t & 7)) << 4));
+      }
+    }
+    uint32_t mq = 0, mk = 0, mv = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      mq = max(mq, __float_as_uint(q[i]) & 0x7fffffffu);
+      mk = max(mk, __float_as_uint(k[i]) & 0x7fffffffu);
+      mv = max(mv, __float_as_uint(v[i]) & 0x7fffffffu);
+    }
+    mq = __reduce_max_sync(0xffffffffu, mq);
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    mv = __reduce_max_sync(0xffffffffu, mv);
+    compute_bar();  // rmax of the previous split has been read by everyone
+    if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
+    compute_bar();
+    {
+      const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
+                     cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+      mq = __reduce_max_sync(0xffffffffu, a);
+      mk = __reduce_max_sync(0xffffffffu, bq);
+      mv = __reduce_max_sync(0xffffffffu, cq);
+    }
+    fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 16 * half, hi);
+      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 32 + 16 * half, lo);
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = row * 128 + ((((4 * half + c) ^ (row & 7))) << 4);
+        *reinterpret_cast<uint4*>(sKh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sKl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    {
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(v[2 * j], fv), __fmul_rn(v[2 * j + 1], fv), hi[j], lo[j]);
+      uint8_t* vh = sVT + vb * (2 * kH16);
+      uint8_t* vl = vh + kH16;
+      const uint32_t atom = (uint32_t)(vtb >> 1) * (64 * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = atom + vd * 128 + ((((4 * (vtb & 1) + c) ^ (vd & 7))) << 4);
+        *reinterpret_cast<uint4*>(vh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(vl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      }
+    }
+    tmem_st_wait();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    compute_bar();
+    tc_fence_after();
+    if (tid == 0) mbar_arrive(xfree);
+  };
+  auto issue_s = [&]() {
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, 128);
+      const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttD / 16; ++ks)
+          mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks, idesc,
+                           (t3 | ks) != 0);
+      mma_commit_elect(barS);
+    }
+  };
+
+
+  // prologue: first unit's projection, split and S
+  float fq = 1.0f, fk = 1.0f, fv = 1.0f;
+  if ((int)blockIdx.x < nheads_total) {
+    epilogue(blockIdx.x, 0);
+    split(0, fq, fk, fv);
+    issue_s();
+  }
+  int it = 0;
+  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+    const uint32_t ph = it & 1;
+    const int nxt = hd + gridDim.x;
+    const int b = hd / heads, h = hd % heads;
+    const float cfq = fq, cfk = fk, cfv = fv;  // this head's scales (split(nxt) overwrites)
+    mbar_wait(barS, ph);
+    tc_fence_after();
+
+    // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
+    float s[64];
+    {
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem + lane_base + half * 64;
+      tmem_ld_32x32b_x32(ta, r0);
+      tmem_ld_32x32b_x32(ta + 32, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        s[j] = __uint_as_float(r0[j]);
+        s[32 + j] = __uint_as_float(r1[j]);
+      }
+    }
+    float mx = -INFINITY;
+    if (seq == kAttT && !causal) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = half * 64 + j;
+        if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
+        mx = fmaxf(mx, s[j]);
+      }
+    }
+    red[half * 128 + row] = mx;
+    compute_bar();
+    mx = fmaxf(red[row], red[128 + row]);
+    // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
+    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
+    const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
+    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
+      s[j] = e;
+      sp[j & 3] = __fadd_rn(sp[j & 3], e);
+    }
+    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+    compute_bar();
+    red[half * 128 + row] = sum;
+    compute_bar();
+    sum = __fadd_rn(red[row], red[128 + row]);
+    // O = (P' V') / (fv sum'), sum' = 2^15 sum
+    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
+    {
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) split_f16x2(s[2 * j], s[2 * j + 1], hi[j], lo[j]);
+      tmem_st_32x32b_x32u(tmem + lane_base + 32 * half, hi);
+      tmem_st_32x32b_x32u(tmem + lane_base + 64 + 32 * half, lo);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    compute_bar();
+    tc_fence_after();
+
+    // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T buffer it & 1 ----
+    if (warp == 0) {
+      const uint32_t idesc = make_idesc_f16(128, kAttD);
+      const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
+      const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
+#pragma unroll
+      for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+        for (int ks = 0; ks < kAttT / 16; ++ks) {
+          const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
+          mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                           (t3 | ks) != 0);
+        }
+      mma_commit_elect(barO);
+    }
+    // ---- the next unit's projection epilogue and split run while the tensor
+    //      core computes P V (the GEMM of the unit after streams meanwhile) ----
+    if (nxt < nheads_total) {
+      epilogue(nxt, it + 1);
+      split((it + 1) & 1, fq, fk, fv);
+    }
+    mbar_wait(barO, ph);
+    tc_fence_after();
+    if (nxt < nheads_total) issue_s();  // P of this head is consumed: S of the next may overwrite it
+    {
+      uint32_t r0[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
+      if (row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
+                          __uint_as_float(r0[j + 3]));
+      }
+    }
+    tc_fence_before();
+    compute_bar();  // O read out: the next P V may overwrite it
+    tc_fence_after();
+  }
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
                   int box_cols, int box_rows, CUtensorMapSwizzle sw);
+int make_tmap_2d(CUtensorMap* tm, CUtensorMapDataType dt, const void* base, int64_t rows, int64_t cols,
+                 int64_t ld_bytes, int box_cols, int box_rows, CUtensorMapSwizzle sw,
+                 CUtensorMapL2promotion promo);
 
 }  // namespace zq
 
@@ -1665,6 +2060,49 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   }
   if (e != cudaSuccess) {
     set_error("attention launch: %s", cudaGetErrorString(e));
+    return ZQ_ERR_CUDA;
+  }
+  return ZQ_OK;
+}
+
+// Fused W8A8 QKV projection + attention (encoder, dynamic token-wise activations):
+// ctx == zq_attention_f32(zq_linear(xq, w_qkv) as f32) bit for bit, without the
+// [T, 3d] f32 QKV round trip.  ZQ_ERR_UNSUPPORTED outside head_dim 64, seq <= 128,
+// d a multiple of 128 (the caller runs the two kernels).
+extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* token_scales, const int8_t* w_qkv,
+                                int64_t ld_w, const float* w_row_scales, const float* bias, int batch, int seq,
+                                int heads, int head_dim, int causal, float scale, float* ctx, int64_t ld_ctx,
+                                void* stream) {
+  ZQ_CHECK_ARG(batch >= 1 && seq >= 1 && heads >= 1 && head_dim >= 1, ZQ_ERR_SHAPE, "bad attention shape");
+  ZQ_CHECK_ARG(xq && token_scales && w_qkv && w_row_scales && ctx, ZQ_ERR_USAGE, "null operand");
+  const int dmodel = heads * head_dim;
+  ZQ_CHECK_ARG(head_dim == kAttD && seq <= kAttT && dmodel % 128 == 0, ZQ_ERR_UNSUPPORTED,
+               "fused QKV attention needs head_dim 64, seq <= 128 and d a multiple of 128");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  ZQ_CHECK_ARG(ld_x % 16 == 0 && ld_w % 16 == 0 && ld_ctx % 4 == 0 && ld_x >= dmodel && ld_w >= dmodel &&
+                   ld_ctx >= dmodel && al16(xq) && al16(w_qkv) && al16(w_row_scales) && al16(ctx) &&
+                   (bias == nullptr || al16(bias)),
+               ZQ_ERR_UNSUPPORTED, "fused QKV attention operands must be 16-byte aligned");
+  const int64_t M = (int64_t)batch * seq;
+  CUtensorMap tmX, tmW;
+  int rc = make_tmap_2d(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, xq, M, dmodel, ld_x, 128, 128,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (rc == ZQ_OK)
+    rc = make_tmap_2d(&tmW, CU_TENSOR_MAP_DATA_TYPE_UINT8, w_qkv, 3LL * dmodel, dmodel, ld_w, 128, kAttD,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (rc != ZQ_OK) return rc;
+  static ZqDeviceOnce attr_once;
+  attr_once([&](int) {
+    cudaFuncSetAttribute(qkv_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQaSmem);
+  });
+  const int total = batch * heads;
+  const int nsm = zq_num_sms();
+  const int grid = total < nsm ? total : nsm;
+  cudaError_t e = launch_kernel(qkv_attention_kernel, dim3(grid), dim3(320), kQaSmem,
+                                reinterpret_cast<cudaStream_t>(stream), 1, tmX, tmW, token_scales, w_row_scales, bias,
+                                (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx, total);
+  if (e != cudaSuccess) {
+    set_error("fused QKV attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
   }
   return ZQ_OK;

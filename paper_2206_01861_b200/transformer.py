@@ -539,6 +539,9 @@ class EncoderEngine:
         # LN work runs on the GEMM's 8 epilogue warps per SM instead of a full-occupancy
         # row kernel): opt-in with ZQ_FUSE_LN=1
         self._fuse_ln = os.environ.get("ZQ_FUSE_LN", "0") == "1"
+        # QKV GEMM + attention in one kernel (zq_qkv_attention): the [t, 3d] f32
+        # QKV activation stays in the SM; ZQ_FUSE_QKV=0 runs the two kernels
+        self._fuse_qkv = os.environ.get("ZQ_FUSE_QKV", "1") == "1"
 
     @property
     def tokens(self) -> int:
@@ -566,6 +569,25 @@ class EncoderEngine:
             N.stream_ptr())
         if rc == N.ZQ_ERR_UNSUPPORTED:
             self._fuse_ln = False
+            return False
+        N.check(rc)
+        return True
+
+    def _qkv_attention(self, q, s, blk: DeviceBlock, ctx) -> bool:
+        """QKV linear + attention fused (zq_qkv_attention, bit-identical to the
+        two kernels); False when the shape is not fusable."""
+        if not self._fuse_qkv or blk.w_qkv.bits != 8:
+            return False
+        t, d = q.shape[0], self.embedding.shape[1]
+        dh = d // blk.num_heads
+        wp, ldw, _ = blk.w_qkv.weight_operand()
+        scale = float(np.float32(1.0 / math.sqrt(dh)))
+        rc = N.call_rc(
+            "zq_qkv_attention", q.data_ptr(), q.stride(0), s.data_ptr(), wp, ldw, blk.w_qkv.row_scales().data_ptr(), N.ptr(blk.b_qkv),
+            self.batch, self.seq, blk.num_heads, dh, int(self.causal), scale, ctx.data_ptr(), ctx.stride(0),
+            N.stream_ptr())
+        if rc == N.ZQ_ERR_UNSUPPORTED:
+            self._fuse_qkv = False
             return False
         N.check(rc)
         return True
@@ -602,10 +624,11 @@ class EncoderEngine:
         self._tok_quant(B["x"], B["xq"], B["sx"])
         x, xq, sx = B["x"], B["xq"], B["sx"]
         for blk in self.blocks:
-            self._linear(xq, sx, blk.w_qkv, blk.b_qkv, B["qkv"])
-            qkv = B["qkv"]
-            attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads, self.causal,
-                      self.batch, out=B["ctx"])
+            if not self._qkv_attention(xq, sx, blk, B["ctx"]):
+                self._linear(xq, sx, blk.w_qkv, blk.b_qkv, B["qkv"])
+                qkv = B["qkv"]
+                attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], blk.num_heads, self.causal,
+                          self.batch, out=B["ctx"])
             self._tok_quant(B["ctx"], B["cq"], B["sc"])
             # h = LN1(x + O-proj) and its quantization, fused into the O GEMM when possible
             if not self._linear_ln(B["cq"], B["sc"], blk.w_o, blk.b_o, x, blk.ln1_gamma, blk.ln1_beta, B["h"],
