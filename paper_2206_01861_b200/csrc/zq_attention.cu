@@ -1559,52 +1559,78 @@ __global__ void __launch_bounds__(256, 1)
 // Fused QKV projection + attention (encoder, seq <= 128, head_dim 64).
 // One CTA per (sequence, head) unit computes that unit's 128 x 192 slice of the
 // W8A8 QKV linear (tokens b*seq.., weight rows {Q, K, V} x [64h, 64h+64)) with
-// tcgen05 kind::i8 into TMEM, dequantizes it exactly as the GEMM epilogue does
-// (((f32(acc) * s_tok) * s_w) + b, pkg/src/lowbit/igemm.py:131-139 — the values
-// zq_linear writes), and lays it out as the raw f32 Q | K | V tiles that
-// attention_f16_kernel loads by TMA; the attention then runs as in that kernel.
-// The [T, 3d] f32 QKV activation never leaves the SM: ctx is bit-identical to
-// zq_linear + zq_attention_f32 (tests/test_qkv_attention_gpu.py).
-//   warps 0-7: attention (attention_f16_kernel's code) + the GEMM epilogue
-//   warp 8   : TMA producer of the GEMM operands (3-stage ring over the raw region)
+// tcgen05 kind::i8 into TMEM, dequantizes it from TMEM exactly as the GEMM
+// epilogue does (((f32(acc) * s_tok) * s_w) + b, pkg/src/lowbit/igemm.py:131-139 —
+// the values zq_linear writes) straight into attention_f16_kernel's hi/lo split;
+// the attention then runs as in that kernel.  The [T, 3d] f32 QKV activation never
+// leaves the SM: ctx is bit-identical to zq_linear + zq_attention_f32
+// (tests/test_qkv_attention_gpu.py).
+//   warps 0-7: GEMM epilogue + split, attention (attention_f16_kernel's code)
+//   warp 8   : TMA producer of the GEMM operands (3-stage ring)
 //   warp 9   : GEMM MMA issuer
-//   smem: X = ring (3 x [A 128 x 128 B | B 192 x 128 B], 120 KB) or raw Q | K | V
-//         (f32, 96 KB) | K hi | K lo | 2 x (V^T hi | V^T lo) | barriers
+//   smem: ring (3 x [A 128 x 128 B | B 192 x 128 B], 120 KB) | K hi | K lo |
+//         2 x (V^T hi | V^T lo) | barriers
 //   TMEM (512 cols): attention's [0, 256) + the GEMM accumulator [256, 448)
-// Pipeline: the GEMM of unit u+1 streams while the attention of unit u runs; the
-// ring is handed back to it by split(u) (barrier xfree).
+// Pipeline: the operands of unit u+1 stream in while unit u's attention runs and
+// its MMAs start as soon as unit u's accumulator has been read (accfree).
 // ---------------------------------------------------------------------------
 constexpr int kQaStages = 3;
 constexpr int kQaStageA = 128 * 128, kQaStageB = 3 * kAttD * 128;
 constexpr int kQaStage = kQaStageA + kQaStageB;  // 40 KB
-constexpr int kQaX = kQaStages * kQaStage;       // 120 KB >= raw Q | K | V (96 KB)
-constexpr int kQaSmem = kQaX + 6 * kH16 + 128 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr int kQaX = kQaStages * kQaStage;       // 120 KB
+constexpr int kQaSc = 2 * 2 * 3 * kAttD * 4;      // [unit parity][scale | bias][Q | K | V][64] f32
+constexpr int kQaSmem = kQaX + 6 * kH16 + kQaSc + 128 + 3 * 8 * 4 + 2 * 128 * 4;
 constexpr uint32_t kQaAcc = 256;
-static_assert(kQaX >= 3 * kRegion, "raw tiles must fit the operand ring");
+
+__device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 __device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// Long waits of the producer / MMA warps: back off between polls so the waiting
+// lane does not take issue slots from the compute warps on its scheduler.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), done;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(128);
+  }
+}
 
 __global__ void __launch_bounds__(320, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                          const float* __restrict__ ts, const float* __restrict__ rs, const float* __restrict__ bias,
                          int M, int seq, int heads, int dmodel, int causal, float scale, float* __restrict__ ctx,
-                         int64_t ld_ctx, int nheads_total) {
+                         int64_t ld_ctx, int nheads_total, unsigned long long* __restrict__ trace,
+                         const __grid_constant__ CUtensorMap tmc, int tma_store, int trigger_late) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sX = sm;
-  uint8_t* sQ = sm;
-  uint8_t* sK = sm + kRegion;
-  uint8_t* sV = sm + 2 * kRegion;
   uint8_t* sKh = sm + kQaX;
   uint8_t* sKl = sKh + kH16;
   uint8_t* sVT = sKl + kH16;  // [2 buffers][hi | lo]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sVT + 4 * kH16);
+  float* sSc = reinterpret_cast<float*>(sVT + 4 * kH16);  // per-unit weight scales and bias
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVT + 4 * kH16 + kQaSc);
   uint64_t* gfull = bars;       // [3] operand stage landed
   uint64_t* gempty = bars + 3;  // [3] operand stage consumed by the MMAs
   uint64_t* accf = bars + 6;    // GEMM accumulator complete
-  uint64_t* xfree = bars + 7;   // raw tiles read (ring and accumulator free)
+  uint64_t* accfree = bars + 7; // accumulator read by the epilogue
   uint64_t* barS = bars + 8;
   uint64_t* barO = bars + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* scf = bars + 10;    // [2] unit parity: scales and bias landed
+  uint64_t* scfree = bars + 12; // [2] unit parity: scales and bias read by epi_split
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
   uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 16);  // [8 warps][3]
   float* red = reinterpret_cast<float*>(rmax + 24);         // [2][128] row partials
 
@@ -1614,7 +1640,7 @@ __global__ void __launch_bounds__(320, 1)
     if (smem_u32(sm) & 1023) __trap();
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
-    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -1622,18 +1648,34 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  pdl_trigger();
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
+  if (tr) tr[0] = gtime();
+  if (!(trigger_late & 1)) pdl_trigger();
   pdl_wait();
+  if (tr) tr[1] = gtime();
 
   if (warp == 8) {  // ===== GEMM operand producer =====
     if (lane == 0) {
       int kc = 0, u = 0;
       for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
-        if (u > 0) mbar_wait(xfree, (u - 1) & 1);
         const int b = hd / heads, h = hd % heads;
+        if ((trigger_late & 2) && u >= 1) mbar_wait(accfree, (u - 1) & 1);  // debug: no operand prefetch
+        {  // the unit's 192 weight-row scales and biases, buffer u & 1 (free once
+           // epi_split(u - 2) has read it)
+          if (u >= 2) mbar_wait_idle(&scfree[u & 1], ((u >> 1) - 1) & 1);
+          float* dst = sSc + (u & 1) * (2 * 3 * kAttD);
+          mbar_arrive_expect_tx(&scf[u & 1], (bias ? 2 : 1) * 3 * kAttD * 4);
+#pragma unroll
+          for (int part = 0; part < 3; ++part) {
+            bulk_load_1d(dst + part * kAttD, rs + part * dmodel + h * kAttD, kAttD * 4, &scf[u & 1]);
+            if (bias) bulk_load_1d(dst + 3 * kAttD + part * kAttD, bias + part * dmodel + h * kAttD, kAttD * 4,
+                                   &scf[u & 1]);
+          }
+        }
         for (int kb = 0; kb < nkb; ++kb, ++kc) {
           const int s = kc % kQaStages;
-          if (kc >= kQaStages) mbar_wait(&gempty[s], ((kc / kQaStages) - 1) & 1);
+          if (kc >= kQaStages) mbar_wait_idle(&gempty[s], ((kc / kQaStages) - 1) & 1);
+          if (trace && kb == 0 && kc / nkb < 4) trace[(size_t)blockIdx.x * 64 + 60 + kc / nkb] = gtime();
           uint8_t* st = sX + s * kQaStage;
           mbar_arrive_expect_tx(&gfull[s], kQaStage);
           tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
@@ -1651,12 +1693,14 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idesc = make_idesc_i8(128, 3 * kAttD);
       int kc = 0, u = 0;
       for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
-        if (u > 0) mbar_wait(xfree, (u - 1) & 1);  // the epilogue has read the accumulator
+        if (u > 0) mbar_wait_idle(accfree, (u - 1) & 1);  // the previous unit's accumulator has been read
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb, ++kc) {
           const int s = kc % kQaStages;
           mbar_wait(&gfull[s], (kc / kQaStages) & 1);
           tc_fence_after();
+          if (trace && kb == nkb - 1 && u < 4) trace[(size_t)blockIdx.x * 64 + 56 + u] = gtime();
+          if (trace && kb == 0 && u < 4) trace[(size_t)blockIdx.x * 64 + 52 + u] = gtime();
           const uint32_t a_addr = smem_u32(sX + s * kQaStage);
           const uint32_t b_addr = a_addr + kQaStageA;
 #pragma unroll
@@ -1676,82 +1720,73 @@ __global__ void __launch_bounds__(320, 1)
   const int row = quarter * 32 + lane;
   const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
 
-  // accumulator of unit (hd, u) -> raw f32 Q | K | V tiles in the SW128 layout of
-  // attention_f16_kernel's TMA boxes (tile part, box j = columns [32j, 32j+32)).
-  // Rows past the last token are zero, as the TMA fill of the unfused path.
-  auto epilogue = [&](int hd, int u) {
-    const int b = hd / heads, h = hd % heads;
-    const int grow = b * seq + row;
-    const bool live = grow < M;
-    const float s_tok = live ? __ldg(ts + grow) : 0.0f;
-    mbar_wait(accf, u & 1);
-    tc_fence_after();
-#pragma unroll 1
-    for (int c3 = 0; c3 < 3; ++c3) {
-      const int cc = half * 3 + c3;  // 32-column chunk of the 192
-      const int part = cc >> 1, box = cc & 1;
-      const int n0 = part * dmodel + h * kAttD + 32 * box;
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + cc * 32, r);
-      tmem_ld_wait();
-      float f[32];
-      const float4* sw4 = reinterpret_cast<const float4*>(rs + n0);
+  // accumulator chunk -> dequantized f32 (((f32(acc) * s_tok) * s_w) + b, the GEMM
+  // epilogue's arithmetic); rows past the last token are 0, as the TMA fill of the
+  // unfused path.
+  auto dequant = [&](uint32_t* r, const float* sw, const float* sb, bool live, float s_tok) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 w = *reinterpret_cast<const float4*>(sw + 4 * j);
+      r[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x));
+      r[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y));
+      r[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z));
+      r[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w));
+    }
+    if (bias != nullptr) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float4 w = __ldg(sw4 + j);
-        f[4 * j + 0] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x);
-        f[4 * j + 1] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y);
-        f[4 * j + 2] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z);
-        f[4 * j + 3] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w);
+        const float4 bb = *reinterpret_cast<const float4*>(sb + 4 * j);
+        r[4 * j + 0] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 0]), bb.x));
+        r[4 * j + 1] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 1]), bb.y));
+        r[4 * j + 2] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 2]), bb.z));
+        r[4 * j + 3] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 3]), bb.w));
       }
-      if (bias != nullptr) {
-        const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 bb = __ldg(b4 + j);
-          f[4 * j + 0] = __fadd_rn(f[4 * j + 0], bb.x);
-          f[4 * j + 1] = __fadd_rn(f[4 * j + 1], bb.y);
-          f[4 * j + 2] = __fadd_rn(f[4 * j + 2], bb.z);
-          f[4 * j + 3] = __fadd_rn(f[4 * j + 3], bb.w);
-        }
-      }
-      uint8_t* dst = sX + part * kRegion + box * (kRegion / 2) + row * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<float4*>(dst + ((c ^ (row & 7)) << 4)) =
-            live ? make_float4(f[4 * c], f[4 * c + 1], f[4 * c + 2], f[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    tc_fence_before();
-    compute_bar();  // raw tiles complete
+    if (!live) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = 0u;
+    }
+  };
+  // x -> f16 hi in the low half, f16 lo (x - hi) in the high half (split_f16x2's
+  // arithmetic per element)
+  auto hl16 = [](float x) -> uint32_t {
+    const __half hh = __float2half_rn(x);
+    const __half ll = __float2half_rn(__fsub_rn(x, __half2float(hh)));
+    return (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
   };
 
-
-  // raw tiles (written by epilogue) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo
-  // (buffer vb) in smem; returns the unit's three power-of-two scales and hands
-  // the raw region back to the GEMM (xfree).  As attention_f16_kernel's split.
-  auto split = [&](int vb, float& fq, float& fk, float& fv) {
-    float q[32], k[32], v[32];
+  // accumulator of unit (hd, u) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo (buffer
+  // vb) in smem, with attention_f16_kernel's per-tile power-of-two scales (the
+  // tile maxima do not depend on which thread holds which element).  Thread
+  // (row, half) holds columns [32 half, 32 half + 32) of its row of Q, K and V;
+  // V^T is written as token pairs exchanged between adjacent lanes.  The
+  // accumulator goes back to the GEMM (accfree) as soon as it has been read.
+  // s_tok: the token scale of this thread's row of unit hd (0 past the last token),
+  // loaded by the caller ahead of time.
+  auto epi_split = [&](int hd, int u, int vb, float s_tok, float& fq, float& fk, float& fv,
+                       unsigned long long* stamp) {
+    const bool live = (hd / heads) * seq + row < M;
+    uint32_t qa[32], ka[32], va[32];
+    mbar_wait(accf, u & 1);
+    tc_fence_after();
+    if (stamp) *stamp = gtime();
+    unsigned long long* ss = (stamp && u == 1) ? tr + 40 : nullptr;
+    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + 32 * half, qa);
+    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + kAttD + 32 * half, ka);
+    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + 2 * kAttD + 32 * half, va);
+    if (tid == 0 && tma_store && u >= 2) bulk_wait_read0();  // O staging (V^T buffer vb) read out
+    mbar_wait(&scf[u & 1], (u >> 1) & 1);
+    tmem_ld_wait();
+    if (ss) ss[0] = gtime();
     {
-      const uint8_t* qr = sQ + half * (kRegion / 2) + row * 128;
-      const uint8_t* kr = sK + half * (kRegion / 2) + row * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 a = *reinterpret_cast<const float4*>(qr + ((c ^ (row & 7)) << 4));
-        const float4 bb = *reinterpret_cast<const float4*>(kr + ((c ^ (row & 7)) << 4));
-        q[4 * c] = a.x, q[4 * c + 1] = a.y, q[4 * c + 2] = a.z, q[4 * c + 3] = a.w;
-        k[4 * c] = bb.x, k[4 * c + 1] = bb.y, k[4 * c + 2] = bb.z, k[4 * c + 3] = bb.w;
-      }
+      const float* sw = sSc + (u & 1) * (2 * 3 * kAttD) + 32 * half;
+      dequant(qa, sw, sw + 3 * kAttD, live, s_tok);
+      dequant(ka, sw + kAttD, sw + 4 * kAttD, live, s_tok);
+      dequant(va, sw + 2 * kAttD, sw + 5 * kAttD, live, s_tok);
     }
-    const int vd = tid & 63, vtb = tid >> 6;  // V^T row (head dim) and 32-token block
-    {
-      const uint8_t* vc = sV + (vd >> 5) * (kRegion / 2) + (vd & 3) * 4;
-      const int jc = (vd & 31) >> 2;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int t = 32 * vtb + i;
-        v[i] = *reinterpret_cast<const float*>(vc + t * 128 + ((jc ^ (t & 7)) << 4));
-      }
-    }
+    float* q = reinterpret_cast<float*>(qa);
+    float* k = reinterpret_cast<float*>(ka);
+    float* v = reinterpret_cast<float*>(va);
     uint32_t mq = 0, mk = 0, mv = 0;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -1762,9 +1797,15 @@ __global__ void __launch_bounds__(320, 1)
     mq = __reduce_max_sync(0xffffffffu, mq);
     mk = __reduce_max_sync(0xffffffffu, mk);
     mv = __reduce_max_sync(0xffffffffu, mv);
+    if (ss) ss[1] = gtime();
     compute_bar();  // rmax of the previous split has been read by everyone
     if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
-    compute_bar();
+    tc_fence_before();
+    compute_bar();  // also: every thread has read the accumulator and the scales
+    if (tid == 0) {
+      if (!(trigger_late & 4)) mbar_arrive(accfree);
+      mbar_arrive(&scfree[u & 1]);
+    }
     {
       const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
                      cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
@@ -1773,6 +1814,7 @@ __global__ void __launch_bounds__(320, 1)
       mv = __reduce_max_sync(0xffffffffu, cq);
     }
     fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
+    if (ss) ss[2] = gtime();
     {
       uint32_t hi[16], lo[16];
 #pragma unroll
@@ -1792,25 +1834,38 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     {
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(v[2 * j], fv), __fmul_rn(v[2 * j + 1], fv), hi[j], lo[j]);
+      if (ss) ss[3] = gtime();
+      // V^T [64 dims][128 tokens] f16, 2 atoms of [64 x 128 B]: token t of dim d at
+      // atom t / 64, row d, 16-byte chunk ((t % 64) / 8) ^ (d % 8), element t % 8.
+      // The even lane of a token pair writes dim kk, the odd lane dim 16 + (kk ^ 4)
+      // (their swizzled chunks differ: no bank conflict between the two halves).
       uint8_t* vh = sVT + vb * (2 * kH16);
       uint8_t* vl = vh + kH16;
-      const uint32_t atom = (uint32_t)(vtb >> 1) * (64 * 128);
+      const bool odd = lane & 1;
+      const int t0 = row & ~1;
+      const uint32_t tbase = (uint32_t)(t0 >> 6) * (64 * 128) + (uint32_t)(t0 & 7) * 2;
+      const int tch = (t0 & 63) >> 3;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t off = atom + vd * 128 + ((((4 * (vtb & 1) + c) ^ (vd & 7))) << 4);
-        *reinterpret_cast<uint4*>(vh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-        *reinterpret_cast<uint4*>(vl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      for (int kk = 0; kk < 16; ++kk) {
+        const int dm = kk, dp = 16 + (kk ^ 4);
+        const uint32_t e_dm = hl16(__fmul_rn(v[dm], fv)), e_dp = hl16(__fmul_rn(v[dp], fv));
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, odd ? e_dm : e_dp, 1);
+        const uint32_t mine = odd ? e_dp : e_dm;
+        const uint32_t ev = odd ? recv : mine, od = odd ? mine : recv;  // tokens t0, t0 + 1
+        const int d = 32 * half + (odd ? dp : dm);
+        const uint32_t off = tbase + (uint32_t)d * 128 + (uint32_t)((tch ^ (d & 7)) << 4);
+        *reinterpret_cast<uint32_t*>(vh + off) = (ev & 0xffffu) | (od << 16);
+        *reinterpret_cast<uint32_t*>(vl + off) = (ev >> 16) | (od & 0xffff0000u);
       }
     }
+    if (ss) ss[4] = gtime();
     tmem_st_wait();
     fence_proxy_async_smem();
     tc_fence_before();
     compute_bar();
     tc_fence_after();
-    if (tid == 0) mbar_arrive(xfree);
+    if ((trigger_late & 4) && tid == 0) mbar_arrive(accfree);  // debug: GEMM after the whole split
+    if (ss) ss[5] = gtime();
   };
   auto issue_s = [&]() {
     if (warp == 0) {
@@ -1828,20 +1883,30 @@ __global__ void __launch_bounds__(320, 1)
 
 
   // prologue: first unit's projection, split and S
+  auto token_scale = [&](int hd) {
+    const int grow = (hd / heads) * seq + row;
+    return hd < nheads_total && grow < M ? __ldg(ts + grow) : 0.0f;
+  };
   float fq = 1.0f, fk = 1.0f, fv = 1.0f;
-  if ((int)blockIdx.x < nheads_total) {
-    epilogue(blockIdx.x, 0);
-    split(0, fq, fk, fv);
-    issue_s();
-  }
-  int it = 0;
-  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+  // it = -1: the first unit's projection and split only; it >= 0: unit hd's attention,
+  // with unit nxt's projection and split under its P V.  One loop body: a single copy
+  // of epi_split in the instruction stream (the prologue warms it).
+  for (int it = -1;; ++it) {
+    const bool cur = it >= 0;
+    const int hd = (int)blockIdx.x + it * (int)gridDim.x;
+    const int nxt = hd + (int)gridDim.x;
+    if (cur ? hd >= nheads_total : nxt >= nheads_total) break;
     const uint32_t ph = it & 1;
-    const int nxt = hd + gridDim.x;
     const int b = hd / heads, h = hd % heads;
     const float cfq = fq, cfk = fk, cfv = fv;  // this head's scales (split(nxt) overwrites)
+    const float s_tok_nxt = token_scale(nxt);  // in flight during the softmax
+    unsigned long long* ti = (tr && cur && it < 6) ? tr + 8 + it * 8 : nullptr;
+    if (ti) ti[0] = gtime();
+    float oscale = 0.0f;
+    if (cur) {
     mbar_wait(barS, ph);
     tc_fence_after();
+    if (ti) ti[1] = gtime();
 
     // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
     float s[64];
@@ -1888,7 +1953,7 @@ __global__ void __launch_bounds__(320, 1)
     compute_bar();
     sum = __fadd_rn(red[row], red[128 + row]);
     // O = (P' V') / (fv sum'), sum' = 2^15 sum
-    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
+    oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
     {
       uint32_t hi[32], lo[32];
 #pragma unroll
@@ -1900,6 +1965,7 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_before();
     compute_bar();
     tc_fence_after();
+    if (ti) ti[2] = gtime();
 
     // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T buffer it & 1 ----
     if (warp == 0) {
@@ -1916,22 +1982,34 @@ __global__ void __launch_bounds__(320, 1)
         }
       mma_commit_elect(barO);
     }
+    }  // cur
     // ---- the next unit's projection epilogue and split run while the tensor
     //      core computes P V (the GEMM of the unit after streams meanwhile) ----
     if (nxt < nheads_total) {
-      epilogue(nxt, it + 1);
-      split((it + 1) & 1, fq, fk, fv);
+      epi_split(nxt, it + 1, (it + 1) & 1, s_tok_nxt, fq, fk, fv, ti ? ti + 3 : (tr && !cur) ? tr + 2 : nullptr);
+      if (ti) ti[4] = gtime();
+      if (tr && !cur) tr[3] = gtime();
     }
-    mbar_wait(barO, ph);
-    tc_fence_after();
+    if (cur) {
+      mbar_wait(barO, ph);
+      tc_fence_after();
+      if (ti) ti[5] = gtime();
+    }
     if (nxt < nheads_total) issue_s();  // P of this head is consumed: S of the next may overwrite it
+    if (!cur) continue;
     {
       uint32_t r0[32];
       tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
-      if (row < seq) {
+      if (tma_store) {  // stage in this unit's V^T buffer (P V is done with it), SW128 f32 boxes
+        uint8_t* st = sVT + (it & 1) * (2 * kH16) + half * kH16 + row * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<uint4*>(st + ((cc ^ (row & 7)) << 4)) =
+              make_uint4(r0[4 * cc], r0[4 * cc + 1], r0[4 * cc + 2], r0[4 * cc + 3]);
+      } else if (row < seq) {
         float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
 #pragma unroll
         for (int j = 0; j < 32; j += 4)
@@ -1940,10 +2018,20 @@ __global__ void __launch_bounds__(320, 1)
                           __uint_as_float(r0[j + 3]));
       }
     }
+    if (tma_store) fence_proxy_async_smem();
     tc_fence_before();
     compute_bar();  // O read out: the next P V may overwrite it
     tc_fence_after();
+    if (tma_store && tid == 0) {
+      const uint8_t* st = sVT + (it & 1) * (2 * kH16);
+      tma_store_2d(&tmc, st, h * kAttD, b * seq);
+      tma_store_2d(&tmc, st + kH16, h * kAttD + 32, b * seq);
+      bulk_commit();
+    }
+    if (ti) ti[6] = gtime();
   }
+  if (tma_store && tid == 0) bulk_wait0();
+  if (trigger_late & 1) pdl_trigger();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
@@ -2065,6 +2153,15 @@ extern "C" int zq_attention_f32(const float* qkv, int64_t ld_qkv, int batch, int
   return ZQ_OK;
 }
 
+static int qa_trigger_late() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZQ_QA_LATE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 // Fused W8A8 QKV projection + attention (encoder, dynamic token-wise activations):
 // ctx == zq_attention_f32(zq_linear(xq, w_qkv) as f32) bit for bit, without the
 // [T, 3d] f32 QKV round trip.  ZQ_ERR_UNSUPPORTED outside head_dim 64, seq <= 128,
@@ -2095,12 +2192,19 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   attr_once([&](int) {
     cudaFuncSetAttribute(qkv_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQaSmem);
   });
+  // seq == 128: whole 128-row boxes belong to one sequence, so O leaves by bulk TMA stores
+  CUtensorMap tmc;
+  int tma_store = 0;
+  if (seq == kAttT && (ld_ctx * 4) % 16 == 0)
+    tma_store = make_tmap_f32(&tmc, ctx, M, dmodel, ld_ctx * 4, 32, kAttT, CU_TENSOR_MAP_SWIZZLE_128B) == ZQ_OK;
+  if (!tma_store) memset(&tmc, 0, sizeof(tmc));
   const int total = batch * heads;
   const int nsm = zq_num_sms();
   const int grid = total < nsm ? total : nsm;
   cudaError_t e = launch_kernel(qkv_attention_kernel, dim3(grid), dim3(320), kQaSmem,
                                 reinterpret_cast<cudaStream_t>(stream), 1, tmX, tmW, token_scales, w_row_scales, bias,
-                                (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx, total);
+                                (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
+                                tma_store, qa_trigger_late());
   if (e != cudaSuccess) {
     set_error("fused QKV attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;

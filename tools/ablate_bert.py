@@ -33,9 +33,34 @@ def time_graph(eng, reps=20):
     return ts[len(ts) // 2]
 
 
+def qkv_ablation(eng):
+    """In-graph cost of QKV projection + attention: fused kernel vs the two kernels."""
+    d = eng.embedding.shape[1]
+    orig_lin, orig_att, orig_fused = eng._linear, T.attention, eng._qkv_attention
+    for fused in (True, False):
+        eng._fuse_qkv = fused
+        eng._graph = None
+        base = time_graph(eng)
+        if fused:
+            eng._qkv_attention = lambda *a, **k: True
+        else:
+            eng._linear = lambda q, s, w, b, o: None if w.rows == 3 * d else orig_lin(q, s, w, b, o)
+            T.attention = lambda *a, **k: None
+        eng._graph = None
+        t = time_graph(eng)
+        eng._linear, T.attention, eng._qkv_attention = orig_lin, orig_att, orig_fused
+        print(f"{'fused' if fused else 'two-kernel'} QKV+attention: forward {base * 1e3:.1f} us, without "
+              f"{t * 1e3:.1f} us -> in-graph cost {(base - t) * 1e3:.1f} us ({(base - t) * 1e3 / len(eng.blocks):.2f} per layer)")
+    eng._fuse_qkv = True
+    eng._graph = None
+
+
 def main():
     eng = bench.build_engine(torch)
     eng._bufs["ids"].copy_(torch.randint(0, bench.BERT["vocab"], (eng.tokens,), device="cuda"))
+    if len(sys.argv) > 1 and sys.argv[1] == "qkv":
+        qkv_ablation(eng)
+        return
     base = time_graph(eng)
     print(f"full forward: {base * 1e3:.1f} us")
     noop = lambda *a, **k: None  # noqa: E731
