@@ -1568,6 +1568,7 @@ __global__ void __launch_bounds__(256, 1)
 //   warps 0-7: GEMM epilogue + split, attention (attention_f16_kernel's code)
 //   warp 8   : TMA producer of the GEMM operands (3-stage ring)
 //   warp 9   : GEMM MMA issuer
+//   warp 10  : attention MMA issuer (S = Q K^T, O = P V)
 //   smem: ring (3 x [A 128 x 128 B | B 192 x 128 B], 120 KB) | K hi | K lo |
 //         2 x (V^T hi | V^T lo) | barriers
 //   TMEM (512 cols): attention's [0, 256) + the GEMM accumulator [256, 448)
@@ -1579,7 +1580,8 @@ constexpr int kQaStageA = 128 * 128, kQaStageB = 3 * kAttD * 128;
 constexpr int kQaStage = kQaStageA + kQaStageB;  // 40 KB
 constexpr int kQaX = kQaStages * kQaStage;       // 120 KB
 constexpr int kQaSc = 2 * 2 * 3 * kAttD * 4;      // [unit parity][scale | bias][Q | K | V][64] f32
-constexpr int kQaSmem = kQaX + 6 * kH16 + kQaSc + 128 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr int kQaSmem = kQaX + 6 * kH16 + kQaSc + 128 + 16 + 3 * 8 * 4 + 2 * 128 * 4;
+constexpr int kQaThreads = 352;
 constexpr uint32_t kQaAcc = 256;
 
 __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -1609,7 +1611,7 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kQaThreads, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                          const float* __restrict__ ts, const float* __restrict__ rs, const float* __restrict__ bias,
                          int M, int seq, int heads, int dmodel, int causal, float scale, float* __restrict__ ctx,
@@ -1630,8 +1632,10 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* barO = bars + 9;
   uint64_t* scf = bars + 10;    // [2] unit parity: scales and bias landed
   uint64_t* scfree = bars + 12; // [2] unit parity: scales and bias read by epi_split
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
-  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 16);  // [8 warps][3]
+  uint64_t* qkr = bars + 14;    // Q, K, V^T of the next unit split (S may be issued)
+  uint64_t* prdy = bars + 15;   // P written (P V may be issued)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 18);  // [8 warps][3]
   float* red = reinterpret_cast<float*>(rmax + 24);         // [2][128] row partials
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1640,7 +1644,7 @@ __global__ void __launch_bounds__(320, 1)
     if (smem_u32(sm) & 1023) __trap();
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
-    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 16; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -1651,38 +1655,57 @@ __global__ void __launch_bounds__(320, 1)
   unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
   if (tr) tr[0] = gtime();
   if (!(trigger_late & 1)) pdl_trigger();
-  pdl_wait();
-  if (tr) tr[1] = gtime();
 
   if (warp == 8) {  // ===== GEMM operand producer =====
     if (lane == 0) {
+      // the unit's 192 weight-row scales and biases -> buffer u & 1 (free once
+      // epi_split(u - 2) has read it)
+      auto load_scales = [&](int h, int u) {
+        if (u >= 2) mbar_wait_idle(&scfree[u & 1], ((u >> 1) - 1) & 1);
+        float* dst = sSc + (u & 1) * (2 * 3 * kAttD);
+        mbar_arrive_expect_tx(&scf[u & 1], (bias ? 2 : 1) * 3 * kAttD * 4);
+#pragma unroll
+        for (int part = 0; part < 3; ++part) {
+          bulk_load_1d(dst + part * kAttD, rs + part * dmodel + h * kAttD, kAttD * 4, &scf[u & 1]);
+          if (bias) bulk_load_1d(dst + 3 * kAttD + part * kAttD, bias + part * dmodel + h * kAttD, kAttD * 4,
+                                 &scf[u & 1]);
+        }
+      };
+      auto load_w = [&](uint8_t* st, int kb, int h, uint64_t* bar) {
+#pragma unroll
+        for (int part = 0; part < 3; ++part)
+          tma_load_2d(st + kQaStageA + part * (kAttD * 128), &tmW, bar, kb * 128, part * dmodel + h * kAttD);
+      };
+      // weights and scales do not depend on the previous kernel: unit 0's first
+      // stages of B go out before griddepcontrol.wait, A (the activations) after it
+      const int npre = nkb < kQaStages ? nkb : kQaStages;
+      if ((int)blockIdx.x < nheads_total) {
+        const int h0 = (int)blockIdx.x % heads;
+        load_scales(h0, 0);
+        for (int kb = 0; kb < npre; ++kb) {
+          mbar_arrive_expect_tx(&gfull[kb], kQaStage);
+          load_w(sX + kb * kQaStage, kb, h0, &gfull[kb]);
+        }
+      }
+      pdl_wait();
+      if (tr) tr[1] = gtime();
       int kc = 0, u = 0;
       for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
         const int b = hd / heads, h = hd % heads;
         if ((trigger_late & 2) && u >= 1) mbar_wait(accfree, (u - 1) & 1);  // debug: no operand prefetch
-        {  // the unit's 192 weight-row scales and biases, buffer u & 1 (free once
-           // epi_split(u - 2) has read it)
-          if (u >= 2) mbar_wait_idle(&scfree[u & 1], ((u >> 1) - 1) & 1);
-          float* dst = sSc + (u & 1) * (2 * 3 * kAttD);
-          mbar_arrive_expect_tx(&scf[u & 1], (bias ? 2 : 1) * 3 * kAttD * 4);
-#pragma unroll
-          for (int part = 0; part < 3; ++part) {
-            bulk_load_1d(dst + part * kAttD, rs + part * dmodel + h * kAttD, kAttD * 4, &scf[u & 1]);
-            if (bias) bulk_load_1d(dst + 3 * kAttD + part * kAttD, bias + part * dmodel + h * kAttD, kAttD * 4,
-                                   &scf[u & 1]);
-          }
-        }
+        if (u > 0) load_scales(h, u);
         for (int kb = 0; kb < nkb; ++kb, ++kc) {
           const int s = kc % kQaStages;
+          uint8_t* st = sX + s * kQaStage;
+          if (u == 0 && kb < npre) {  // B already in flight
+            tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
+            continue;
+          }
           if (kc >= kQaStages) mbar_wait_idle(&gempty[s], ((kc / kQaStages) - 1) & 1);
           if (trace && kb == 0 && kc / nkb < 4) trace[(size_t)blockIdx.x * 64 + 60 + kc / nkb] = gtime();
-          uint8_t* st = sX + s * kQaStage;
           mbar_arrive_expect_tx(&gfull[s], kQaStage);
           tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
-#pragma unroll
-          for (int part = 0; part < 3; ++part)
-            tma_load_2d(st + kQaStageA + part * (kAttD * 128), &tmW, &gfull[s], kb * 128,
-                        part * dmodel + h * kAttD);
+          load_w(st, kb, h, &gfull[s]);
         }
       }
     }
@@ -1715,7 +1738,45 @@ __global__ void __launch_bounds__(320, 1)
     return;
   }
 
+  if (warp == 10) {  // ===== attention MMA issuer: S = Q K^T, O = P V (3-term f16 splits) =====
+    int it = 0;
+    for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+      mbar_wait_idle(qkr, it & 1);                         // Q, K, V^T of unit it split
+      if (it > 0) mbar_wait_idle(barO, (it - 1) & 1);      // P of unit it - 1 consumed
+      tc_fence_after();
+      {
+        const uint32_t idesc = make_idesc_f16(128, 128);
+        const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttD / 16; ++ks)
+            mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks,
+                             idesc, (t3 | ks) != 0);
+        mma_commit_elect(barS);
+      }
+      mbar_wait_idle(prdy, it & 1);                        // P of unit it written
+      tc_fence_after();
+      {
+        const uint32_t idesc = make_idesc_f16(128, kAttD);
+        const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
+        const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttT / 16; ++ks) {
+            const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
+            mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                             (t3 | ks) != 0);
+          }
+        mma_commit_elect(barO);
+      }
+    }
+    return;
+  }
+
   // ===== warps 0-7: GEMM epilogue + attention =====
+  pdl_wait();  // token scales come from the previous kernel
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
   const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
@@ -1864,21 +1925,11 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_before();
     compute_bar();
     tc_fence_after();
-    if ((trigger_late & 4) && tid == 0) mbar_arrive(accfree);  // debug: GEMM after the whole split
-    if (ss) ss[5] = gtime();
-  };
-  auto issue_s = [&]() {
-    if (warp == 0) {
-      const uint32_t idesc = make_idesc_f16(128, 128);
-      const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
-#pragma unroll
-      for (int t3 = 0; t3 < 3; ++t3)
-#pragma unroll
-        for (int ks = 0; ks < kAttD / 16; ++ks)
-          mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks, idesc,
-                           (t3 | ks) != 0);
-      mma_commit_elect(barS);
+    if (tid == 0) {
+      if (trigger_late & 4) mbar_arrive(accfree);  // debug: GEMM after the whole split
+      mbar_arrive(qkr);  // S of this unit may be issued
     }
+    if (ss) ss[5] = gtime();
   };
 
 
@@ -1967,21 +2018,7 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_after();
     if (ti) ti[2] = gtime();
 
-    // ---- O' = P' V' (3 terms), A = P' from TMEM, B = V'^T buffer it & 1 ----
-    if (warp == 0) {
-      const uint32_t idesc = make_idesc_f16(128, kAttD);
-      const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
-      const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
-#pragma unroll
-      for (int t3 = 0; t3 < 3; ++t3)
-#pragma unroll
-        for (int ks = 0; ks < kAttT / 16; ++ks) {
-          const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
-          mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
-                           (t3 | ks) != 0);
-        }
-      mma_commit_elect(barO);
-    }
+    if (tid == 0) mbar_arrive(prdy);  // O' = P' V' is issued by warp 10
     }  // cur
     // ---- the next unit's projection epilogue and split run while the tensor
     //      core computes P V (the GEMM of the unit after streams meanwhile) ----
@@ -1995,7 +2032,6 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       if (ti) ti[5] = gtime();
     }
-    if (nxt < nheads_total) issue_s();  // P of this head is consumed: S of the next may overwrite it
     if (!cur) continue;
     {
       uint32_t r0[32];
@@ -2201,7 +2237,7 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   const int total = batch * heads;
   const int nsm = zq_num_sms();
   const int grid = total < nsm ? total : nsm;
-  cudaError_t e = launch_kernel(qkv_attention_kernel, dim3(grid), dim3(320), kQaSmem,
+  cudaError_t e = launch_kernel(qkv_attention_kernel, dim3(grid), dim3(kQaThreads), kQaSmem,
                                 reinterpret_cast<cudaStream_t>(stream), 1, tmX, tmW, token_scales, w_row_scales, bias,
                                 (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
                                 tma_store, qa_trigger_late());
