@@ -484,7 +484,14 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
     }
   } else {
     // ===================== epilogue (both CTAs, own 128 rows) =====================
-    pdl_wait();
+    // The first pass over the loop body is a dry run of the first tile's epilogue
+    // (accumulator buffer 1, which that tile does not use; staging writes only, no
+    // stores, no barrier traffic) made before griddepcontrol.wait: it pulls the
+    // epilogue's instructions into the SM's instruction cache while the CTA waits
+    // for the previous kernel, instead of on the first real tile (measured in the
+    // BERT graph: first-tile epilogue 5.6 vs 3.7 us for the later tiles).
+    bool dry = !(p.debug & 4) && unit0 < num_units && p.tma_out;
+    if (!dry) pdl_wait();
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int COLS = BN / 2;
@@ -493,7 +500,7 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
     if (p.tma_out && lane == 0) prefetch_tmap(&tmC);
     int acc = 0, acc_phase = 0, lt = 0;
     const bool stamp = tr && warp == 2 && lane == 0;
-    for (int u = unit0; u < num_units; u += nunits_grid, ++lt) {
+    for (int u = unit0; u < num_units;) {
       int mt, nt;
       unit_coords(u, mt, nt);
       const int m0 = mt * (2 * BLOCK_M) + rank * BLOCK_M;
@@ -502,16 +509,18 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
       const int row = row0 + lane;
       float s_tok = p.static_scale;
       if (KIND != OUT_S32 && p.token_scales != nullptr && row < p.M) s_tok = __ldg(p.token_scales + row);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      if (stamp && lt < 15) tr[4 + 4 * lt] = gtime();
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * COLS;
+      if (!dry) {
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        if (stamp && lt < 15) tr[4 + 4 * lt] = gtime();
+      }
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (dry ? 1 : acc) * BN + half * COLS;
 #pragma unroll 1
       for (int c = 0; c < COLS; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c, r);
         tmem_ld_wait();
-        if (c + 32 == COLS) {
+        if (c + 32 == COLS && !dry) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty_bar[acc]));
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
           if (!(p.debug & 2)) epi_chunk_smem<KIND>(r, s_tok, p.row_scales, p.bias, col0, p.N, sb, lane);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0 && !(p.debug & 1)) {
+          if (lane == 0 && !(p.debug & 1) && !dry) {
             tma_store_2d(&tmC, sb, col0, row0);
             if (p.kv_rows_per_seq > 0 && col0 >= p.kv_dl) {
               // prefill: the k / v columns of these 32 token rows also go to the KV
@@ -544,11 +553,18 @@ __global__ void __launch_bounds__(Gemm2Cfg<BN>::NUM_THREADS, 1)
                                col0, p.N);
         }
       }
+      if (dry) {  // the same unit again, for real
+        dry = false;
+        pdl_wait();
+        continue;
+      }
       if (stamp && lt < 15) tr[5 + 4 * lt] = gtime();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
+      u += nunits_grid;
+      ++lt;
     }
     if (lane == 0) bulk_wait0();  // all output stores complete before exit
     if (stamp) tr[63] = gtime();
