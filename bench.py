@@ -315,8 +315,9 @@ def gemm_roofline(torch, eng, peaks, basis):
             "launches_per_step": n_l, "per_launch_us": 1e6 * t_per_pass / n_l,
             "timing": "one forward's linears replayed back to back in a CUDA graph, CUDA events on the replay stream",
             "algorithmic_bytes_per_launch": nbytes / n_l,
-            "bound_basis": "per launch max(ops / P_int8, bytes / B_hbm): the f32 outputs make QKV, O and h4h "
-                           "HBM-bound and 4hh tensor-bound at BERT-base shapes; bytes dominate the sum",
+            "bound_basis": "per launch max(ops / P_int8, bytes / B_hbm): the f32 outputs make O and h4h "
+                           "HBM-bound and 4hh tensor-bound at BERT-base shapes (the QKV projection runs inside "
+                           "the fused QKV + attention kernel, row_kernels.qkv_attention); bytes dominate the sum",
             "tensor_tops": ops / t_per_pass / 1e12, "tensor_peak": p_int8 / 1e12,
             "frac_of_per_launch_roofline": t_roof / t_per_pass,
             "fabric_roofline": {
@@ -391,6 +392,31 @@ def row_kernel_costs(torch, eng, peaks):
         out[name] = {"launches_per_forward": nl, "in_graph_us_per_launch": 1e6 * per,
                      "algorithmic_bytes_per_launch": nbytes, "achieved_GBps": nbytes / per / 1e9,
                      "frac_of_hbm": nbytes / per / 1e9 / peaks["hbm_gbs"]}
+    if eng._fuse_qkv:
+        # fused QKV projection + attention (zq_qkv_attention): bounded by its tensor
+        # work (int8 GEMM at P_int8 plus the 3-term f16 S and P V products at the
+        # bf16 peak) since its bytes (x int8, W_qkv int8, ctx f32) are few
+        orig = eng._qkv_attention
+        eng._qkv_attention = lambda *a, **k: True
+        try:
+            t_without = time_graph()
+        finally:
+            eng._qkv_attention = orig
+        nl = BERT["layers"]
+        per = max(base - t_without, 1e-9) / nl
+        units = BERT["batch"] * BERT["heads"]
+        i8_ops = 2 * t * d * 3 * d
+        f16_flops = units * 2 * 3 * 2 * 128 * 128 * (d // BERT["heads"])
+        nbytes = t * d + 3 * d * d + 4 * 6 * d + 4 * t + 4 * t * d
+        t_bound = max(i8_ops / int8_peak(peaks) + f16_flops / (peaks["bf16_tflops"] * 1e12),
+                      nbytes / (peaks["hbm_gbs"] * 1e9))
+        out["qkv_attention"] = {
+            "kernel": "qkv_attention_kernel (W8A8 QKV GEMM tcgen05 kind::i8 + fp16 two-term attention, one "
+                      "(sequence, head) unit per CTA step; the f32 QKV never reaches HBM)",
+            "launches_per_forward": nl, "in_graph_us_per_launch": 1e6 * per,
+            "int8_ops_per_launch": i8_ops, "f16_flops_per_launch": f16_flops,
+            "algorithmic_bytes_per_launch": nbytes, "bound_us": 1e6 * t_bound, "frac_of_roofline": t_bound / per,
+            "bound_basis": "int8 ops / P_int8 + f16 flops / bf16 peak (tensor-bound; bytes / B_hbm is smaller)"}
     eng.capture()  # leave the engine with its full graph
     del flush
     return out
@@ -522,6 +548,7 @@ def run_ours(args, rank: int, world: int, dist):
     roof = gemm_roofline(torch, eng, peaks, basis) if rank == 0 else None
     rows = row_kernel_costs(torch, eng, peaks) if rank == 0 and not eng._sub else None
     fused = all(e._fuse_ln for e in (eng._sub or [eng]))
+    fused_qkv = all(e._fuse_qkv for e in (eng._sub or [eng]))
     clocks = clk.summary()
     step_mm = [1000 * min(step_s), 1000 * max(step_s)]
     ids_bytes, out_bytes = int(ids_host.numel() * 8), int(out_host[0].numel() * 4)
@@ -532,7 +559,8 @@ def run_ours(args, rank: int, world: int, dist):
         return
     cores = len(os.sched_getaffinity(0))
     cpu_val, cpu_sample, _ = cpu_reference_sample(cores, 1)
-    launches_per_step = 2 + (7 if fused else 9) * BERT["layers"]  # tok quant + per block + final LN
+    # tok quant + per block (QKV GEMM + attention fused: one launch fewer; linear + LN fused: two fewer) + final LN
+    launches_per_step = 2 + (9 - (1 if fused_qkv else 0) - (2 if fused else 0)) * BERT["layers"]
     line = {
         "metric": "BERT-base W8A8 encoder forward throughput", "value": value, "unit": "seq/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
