@@ -289,6 +289,27 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_heads: int,
     return ctx
 
 
+def fused_qkv_attention(xq: torch.Tensor, token_scales: torch.Tensor, w: QuantizedMatrix, bias, num_heads: int,
+                        causal: bool, batch: int, out: torch.Tensor) -> bool:
+    """quantized_linear(x, W_qkv) then attention (transformer.py:395-440) as one
+    kernel (zq_qkv_attention) for an int8 x with per-token scales: out (ctx) is
+    bit-identical to zq_linear + zq_attention_f32.  False (nothing launched) when
+    the shape is outside the kernel (W4 weights, head_dim != 64, seq > 128,
+    d % 128 != 0); ZQ_FUSE_QKV=0 disables it."""
+    if w.bits != 8 or os.environ.get("ZQ_FUSE_QKV", "1") != "1":
+        return False
+    t, d = xq.shape[0], w.cols
+    if t % batch or d % num_heads:
+        return False
+    dh = d // num_heads
+    wp, ldw, _ = w.weight_operand()
+    scale = float(np.float32(1.0 / math.sqrt(dh)))
+    rc = N.call_rc("zq_qkv_attention", xq.data_ptr(), xq.stride(0), token_scales.data_ptr(), wp, ldw,
+                   w.row_scales().data_ptr(), N.ptr(bias), batch, t // batch, num_heads, dh, int(causal), scale,
+                   out.data_ptr(), out.stride(0), N.stream_ptr())
+    return rc == N.ZQ_OK
+
+
 def _linear_site(x, w: QuantizedMatrix, bias, am, full_act: str = "exact"):
     if isinstance(am, FullAct):
         return igemm.full_linear(x, w, bias, precision=full_act)
@@ -313,8 +334,18 @@ def block_forward(x, block: DeviceBlock, precision: PrecisionConfig, causal: boo
         return _act_mode_for(precision, site, layer, static_scales)
 
     am = mode("attn_in")
-    qkv = _linear_site(xt, block.w_qkv, block.b_qkv, am, full_act)
-    ctx = attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], block.num_heads, causal, batch)
+    ctx = None
+    if isinstance(am, DynamicAct) and am.bits == 8 and block.w_qkv.bits == 8:
+        # W8A8 dynamic: QKV projection + attention in one kernel (bit-identical)
+        xq = quant.quantize_activation_tokenwise(xt, 8)
+        ctx = torch.empty((t, d), dtype=torch.float32, device=xt.device)
+        if not fused_qkv_attention(xq.values, xq.token_scales, block.w_qkv, block.b_qkv, block.num_heads, causal,
+                                   batch, ctx):
+            qkv = igemm.fused_linear(xq, block.w_qkv, block.b_qkv)
+            ctx = attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], block.num_heads, causal, batch)
+    if ctx is None:
+        qkv = _linear_site(xt, block.w_qkv, block.b_qkv, am, full_act)
+        ctx = attention(qkv[:, :d], qkv[:, d: 2 * d], qkv[:, 2 * d:], block.num_heads, causal, batch)
     attn_out = _linear_site(ctx, block.w_o, block.b_o, mode("attn_proj_in"), full_act)
     h = torch.empty_like(xt)
     m_ffc_in = mode("ffc_in")
@@ -576,20 +607,11 @@ class EncoderEngine:
     def _qkv_attention(self, q, s, blk: DeviceBlock, ctx) -> bool:
         """QKV linear + attention fused (zq_qkv_attention, bit-identical to the
         two kernels); False when the shape is not fusable."""
-        if not self._fuse_qkv or blk.w_qkv.bits != 8:
+        if not self._fuse_qkv:
             return False
-        t, d = q.shape[0], self.embedding.shape[1]
-        dh = d // blk.num_heads
-        wp, ldw, _ = blk.w_qkv.weight_operand()
-        scale = float(np.float32(1.0 / math.sqrt(dh)))
-        rc = N.call_rc(
-            "zq_qkv_attention", q.data_ptr(), q.stride(0), s.data_ptr(), wp, ldw, blk.w_qkv.row_scales().data_ptr(), N.ptr(blk.b_qkv),
-            self.batch, self.seq, blk.num_heads, dh, int(self.causal), scale, ctx.data_ptr(), ctx.stride(0),
-            N.stream_ptr())
-        if rc == N.ZQ_ERR_UNSUPPORTED:
+        if not fused_qkv_attention(q, s, blk.w_qkv, blk.b_qkv, blk.num_heads, self.causal, self.batch, ctx):
             self._fuse_qkv = False
             return False
-        N.check(rc)
         return True
 
     def _ln_quant(self, x, res, g, b, ln_out, q, s):
