@@ -3,7 +3,8 @@ ncu --set full --nvtx --nvtx-include "prof/": W8A8 GEMM 8192^3 (f16 out),
 4096x4096x16384, W4A8 CTA pair 8192x4096x1024, weight-only f16 NeoX QKV prefill
 (2048x6144x18432), decode 16x6144x24576 (stream-K + sum epilogue), TMA decode
 attention (NeoX, 16 x 192 keys), token quantize / LN+quant / GeLU+quant at
-4096x3072.  Two warm-up launches each, outside the NVTX range."""
+4096x3072, the fused QKV + attention kernel at the BERT bench shape.  Two
+warm-up launches each, outside the NVTX range."""
 import os
 import sys
 
@@ -69,3 +70,11 @@ y = torch.empty_like(x)
 prof(lambda: quant.quantize_activation_tokenwise(x, 8, check_finite=False))
 prof(lambda: igemm.layer_norm_quantize(x, g, b, 8, residual=r, ln_out=y, check_finite=False))
 prof(lambda: igemm.gelu_quantize(x, 8, check_finite=False))
+# fused W8A8 QKV projection + attention at the BERT-base bench shape (32 x 128, 12 heads)
+from paper_2206_01861_b200 import transformer as T  # noqa: E402
+
+xa = quant.quantize_activation_tokenwise(torch.randn(4096, 768, device="cuda"), 8)
+wqkv = quant.quantize_weight_groupwise(torch.randn(2304, 768, device="cuda") * 0.05, 48, 8)
+bqkv = torch.randn(2304, device="cuda") * 0.1
+cx = torch.empty(4096, 768, device="cuda")
+prof(lambda: T.fused_qkv_attention(xa.values, xa.token_scales, wqkv, bqkv, 12, False, 32, cx))
