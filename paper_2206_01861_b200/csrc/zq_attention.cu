@@ -1808,13 +1808,6 @@ __global__ void __launch_bounds__(kQaThreads, 1)
       for (int j = 0; j < 32; ++j) r[j] = 0u;
     }
   };
-  // x -> f16 hi in the low half, f16 lo (x - hi) in the high half (split_f16x2's
-  // arithmetic per element)
-  auto hl16 = [](float x) -> uint32_t {
-    const __half hh = __float2half_rn(x);
-    const __half ll = __float2half_rn(__fsub_rn(x, __half2float(hh)));
-    return (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
-  };
 
   // accumulator of unit (hd, u) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo (buffer
   // vb) in smem, with attention_f16_kernel's per-tile power-of-two scales (the
@@ -1900,6 +1893,8 @@ __global__ void __launch_bounds__(kQaThreads, 1)
       // atom t / 64, row d, 16-byte chunk ((t % 64) / 8) ^ (d % 8), element t % 8.
       // The even lane of a token pair writes dim kk, the odd lane dim 16 + (kk ^ 4)
       // (their swizzled chunks differ: no bank conflict between the two halves).
+      // An element travels as one word, f16 hi | f16 lo << 16 (split_f16x2 of the
+      // dim pair, then byte permutes).
       uint8_t* vh = sVT + vb * (2 * kH16);
       uint8_t* vl = vh + kH16;
       const bool odd = lane & 1;
@@ -1909,7 +1904,9 @@ __global__ void __launch_bounds__(kQaThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         const int dm = kk, dp = 16 + (kk ^ 4);
-        const uint32_t e_dm = hl16(__fmul_rn(v[dm], fv)), e_dp = hl16(__fmul_rn(v[dp], fv));
+        uint32_t hi2, lo2;  // (hi, lo) of dims dm (low halves) and dp (high halves)
+        split_f16x2(__fmul_rn(v[dm], fv), __fmul_rn(v[dp], fv), hi2, lo2);
+        const uint32_t e_dm = __byte_perm(hi2, lo2, 0x5410), e_dp = __byte_perm(hi2, lo2, 0x7632);
         const uint32_t recv = __shfl_xor_sync(0xffffffffu, odd ? e_dm : e_dp, 1);
         const uint32_t mine = odd ? e_dp : e_dm;
         const uint32_t ev = odd ? recv : mine, od = odd ? mine : recv;  // tokens t0, t0 + 1
@@ -1949,9 +1946,10 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     if (cur ? hd >= nheads_total : nxt >= nheads_total) break;
     const uint32_t ph = it & 1;
     const int b = hd / heads, h = hd % heads;
+    unsigned long long* ti = (tr && cur && it < 6) ? tr + 8 + it * 8 : nullptr;
+    if (ti) ti[7] = gtime();
     const float cfq = fq, cfk = fk, cfv = fv;  // this head's scales (split(nxt) overwrites)
     const float s_tok_nxt = token_scale(nxt);  // in flight during the softmax
-    unsigned long long* ti = (tr && cur && it < 6) ? tr + 8 + it * 8 : nullptr;
     if (ti) ti[0] = gtime();
     float oscale = 0.0f;
     if (cur) {

@@ -52,10 +52,10 @@ print("pdl_wait done", med(tr[:, 1]), "first acc", med(tr[:, 2]), "prologue done
 for u in range(4):
     print(f"unit {u}: producer first load {med(tr[:, 60 + u])}  mma first stage {med(tr[:, 52 + u])}"
           f"  mma last stage {med(tr[:, 56 + u])}")
-names = ["start", "S ready", "P written", "acc(nxt)", "split(nxt) done", "PV done", "end"]
+names = ["start", "S ready", "P written", "acc(nxt)", "split(nxt) done", "PV done", "end", "loop top"]
 ends = []
 for it in range(6):
-    row = tr[:, 8 + it * 8: 8 + it * 8 + 7]
+    row = tr[:, 8 + it * 8: 8 + it * 8 + 8]
     if not (row[:, 0] > 0).any():
         break
     print(f"iter {it} ctas {(row[:, 0] > 0).sum()}", {n: med(row[:, i]) for i, n in enumerate(names)})
