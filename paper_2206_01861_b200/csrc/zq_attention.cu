@@ -704,14 +704,22 @@ __global__ void __launch_bounds__(256, 1)
     // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
     const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
     const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
-    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    // row sum: per 32-key quarter four interleaved partials ((p0 + p1) + (p2 + p3)),
+    // the two quarters of this half added, then the halves ((q0 + q1) + (q2 + q3));
+    // qkv_attention_kernel (16 compute warps, 32 keys per thread) sums in this order
+    float qsum[2];
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
-      s[j] = e;
-      sp[j & 3] = __fadd_rn(sp[j & 3], e);
+    for (int qq = 0; qq < 2; ++qq) {
+      float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = ex2_approx_f(__fmaf_rn(s[32 * qq + j], c, -mxc));
+        s[32 * qq + j] = e;
+        sp[j & 3] = __fadd_rn(sp[j & 3], e);
+      }
+      qsum[qq] = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
     }
-    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+    float sum = __fadd_rn(qsum[0], qsum[1]);
     __syncthreads();
     red[half * 128 + row] = sum;
     __syncthreads();
@@ -1580,9 +1588,42 @@ constexpr int kQaStageA = 128 * 128, kQaStageB = 3 * kAttD * 128;
 constexpr int kQaStage = kQaStageA + kQaStageB;  // 40 KB
 constexpr int kQaX = kQaStages * kQaStage;       // 120 KB
 constexpr int kQaSc = 2 * 2 * 3 * kAttD * 4;      // [unit parity][scale | bias][Q | K | V][64] f32
-constexpr int kQaSmem = kQaX + 6 * kH16 + kQaSc + 128 + 16 + 3 * 8 * 4 + 2 * 128 * 4;
-constexpr int kQaThreads = 352;
+// CW compute warps (8 or 16): TMEM lane quarter warp % 4, column part warp / 4
+template <int CW>
+struct QaCfg {
+  static constexpr int NCQ = CW / 4;          // column parts per row
+  static constexpr int KPT = 128 / NCQ;       // S columns (keys) per thread
+  static constexpr int DPT = kAttD / NCQ;     // Q / K / V / O columns per thread
+  static constexpr int THREADS = (CW + 3) * 32;
+  static constexpr int SMEM = kQaX + 6 * kH16 + kQaSc + 128 + 16 + CW * 3 * 4 + 2 * NCQ * 128 * 4;
+};
 constexpr uint32_t kQaAcc = 256;
+
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+// n (a multiple of 8) consecutive 32-bit TMEM columns of this thread's lane
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c < N; c += 16) tmem_ld_32x32b_x16(taddr + c, r + c);
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* v) {
+#pragma unroll
+  for (int c = 0; c < N; c += 8) tmem_st_32x32b_x8(taddr + c, v + c);
+}
 
 __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1591,7 +1632,8 @@ __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, ui
                : "memory");
 }
 
-__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+template <int CW>
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory"); }
 // Long waits of the producer / MMA warps: back off between polls so the waiting
 // lane does not take issue slots from the compute warps on its scheduler.
 __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
@@ -1611,12 +1653,15 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__global__ void __launch_bounds__(kQaThreads, 1)
+template <int CW>
+__global__ void __launch_bounds__(QaCfg<CW>::THREADS, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                          const float* __restrict__ ts, const float* __restrict__ rs, const float* __restrict__ bias,
                          int M, int seq, int heads, int dmodel, int causal, float scale, float* __restrict__ ctx,
                          int64_t ld_ctx, int nheads_total, unsigned long long* __restrict__ trace,
                          const __grid_constant__ CUtensorMap tmc, int tma_store, int trigger_late) {
+  using Cfg = QaCfg<CW>;
+  constexpr int NCQ = Cfg::NCQ, KPT = Cfg::KPT, DPT = Cfg::DPT;
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sX = sm;
   uint8_t* sKh = sm + kQaX;
@@ -1635,8 +1680,9 @@ __global__ void __launch_bounds__(kQaThreads, 1)
   uint64_t* qkr = bars + 14;    // Q, K, V^T of the next unit split (S may be issued)
   uint64_t* prdy = bars + 15;   // P written (P V may be issued)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
-  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 18);  // [8 warps][3]
-  float* red = reinterpret_cast<float*>(rmax + 24);         // [2][128] row partials
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 18);  // [CW warps][3]
+  float* redm = reinterpret_cast<float*>(rmax + CW * 3);    // [NCQ][128] row partial maxima
+  float* reds = redm + NCQ * 128;                           // [NCQ][128] row partial sums
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkb = dmodel / 128;
@@ -1656,7 +1702,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
   if (tr) tr[0] = gtime();
   if (!(trigger_late & 1)) pdl_trigger();
 
-  if (warp == 8) {  // ===== GEMM operand producer =====
+  if (warp == CW) {  // ===== GEMM operand producer =====
     if (lane == 0) {
       // the unit's 192 weight-row scales and biases -> buffer u & 1 (free once
       // epi_split(u - 2) has read it)
@@ -1711,7 +1757,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     }
     return;
   }
-  if (warp == 9) {  // ===== GEMM MMA issuer =====
+  if (warp == CW + 1) {  // ===== GEMM MMA issuer =====
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_i8(128, 3 * kAttD);
       int kc = 0, u = 0;
@@ -1738,7 +1784,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     return;
   }
 
-  if (warp == 10) {  // ===== attention MMA issuer: S = Q K^T, O = P V (3-term f16 splits) =====
+  if (warp == CW + 2) {  // ===== attention MMA issuer: S = Q K^T, O = P V (3-term f16 splits) =====
     int it = 0;
     for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
       mbar_wait_idle(qkr, it & 1);                         // Q, K, V^T of unit it split
@@ -1775,18 +1821,18 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     return;
   }
 
-  // ===== warps 0-7: GEMM epilogue + attention =====
+  // ===== warps 0 .. CW-1: GEMM epilogue + split, softmax, O =====
   pdl_wait();  // token scales come from the previous kernel
-  const int quarter = warp & 3, half = warp >> 2;
+  const int quarter = warp & 3, cq = warp >> 2;  // TMEM lane quarter, column part
   const int row = quarter * 32 + lane;
   const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
 
-  // accumulator chunk -> dequantized f32 (((f32(acc) * s_tok) * s_w) + b, the GEMM
+  // accumulator columns -> dequantized f32 (((f32(acc) * s_tok) * s_w) + b, the GEMM
   // epilogue's arithmetic); rows past the last token are 0, as the TMA fill of the
   // unfused path.
   auto dequant = [&](uint32_t* r, const float* sw, const float* sb, bool live, float s_tok) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < DPT / 4; ++j) {
       const float4 w = *reinterpret_cast<const float4*>(sw + 4 * j);
       r[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x));
       r[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y));
@@ -1795,7 +1841,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     }
     if (bias != nullptr) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < DPT / 4; ++j) {
         const float4 bb = *reinterpret_cast<const float4*>(sb + 4 * j);
         r[4 * j + 0] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 0]), bb.x));
         r[4 * j + 1] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 1]), bb.y));
@@ -1805,84 +1851,85 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     }
     if (!live) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = 0u;
+      for (int j = 0; j < DPT; ++j) r[j] = 0u;
     }
   };
 
   // accumulator of unit (hd, u) -> Q hi/lo in TMEM, K hi/lo and V^T hi/lo (buffer
   // vb) in smem, with attention_f16_kernel's per-tile power-of-two scales (the
   // tile maxima do not depend on which thread holds which element).  Thread
-  // (row, half) holds columns [32 half, 32 half + 32) of its row of Q, K and V;
-  // V^T is written as token pairs exchanged between adjacent lanes.  The
-  // accumulator goes back to the GEMM (accfree) as soon as it has been read.
-  // s_tok: the token scale of this thread's row of unit hd (0 past the last token),
-  // loaded by the caller ahead of time.
+  // (row, cq) holds columns [DPT cq, DPT cq + DPT) of its row of Q, K and V; V^T is
+  // written as token pairs exchanged between adjacent lanes.  The accumulator
+  // goes back to the GEMM (accfree) as soon as it has been read.  s_tok: the token
+  // scale of this thread's row of unit hd (0 past the last token), loaded ahead.
   auto epi_split = [&](int hd, int u, int vb, float s_tok, float& fq, float& fk, float& fv,
                        unsigned long long* stamp) {
     const bool live = (hd / heads) * seq + row < M;
-    uint32_t qa[32], ka[32], va[32];
+    uint32_t qa[DPT], ka[DPT], va[DPT];
     mbar_wait(accf, u & 1);
     tc_fence_after();
     if (stamp) *stamp = gtime();
     unsigned long long* ss = (stamp && u == 1) ? tr + 40 : nullptr;
-    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + 32 * half, qa);
-    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + kAttD + 32 * half, ka);
-    tmem_ld_32x32b_x32(tmem + lane_base + kQaAcc + 2 * kAttD + 32 * half, va);
+    tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + DPT * cq, qa);
+    tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + kAttD + DPT * cq, ka);
+    tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + 2 * kAttD + DPT * cq, va);
     if (tid == 0 && tma_store && u >= 2) bulk_wait_read0();  // O staging (V^T buffer vb) read out
     mbar_wait(&scf[u & 1], (u >> 1) & 1);
     tmem_ld_wait();
     if (ss) ss[0] = gtime();
     {
-      const float* sw = sSc + (u & 1) * (2 * 3 * kAttD) + 32 * half;
+      const float* sw = sSc + (u & 1) * (2 * 3 * kAttD) + DPT * cq;
       dequant(qa, sw, sw + 3 * kAttD, live, s_tok);
       dequant(ka, sw + kAttD, sw + 4 * kAttD, live, s_tok);
       dequant(va, sw + 2 * kAttD, sw + 5 * kAttD, live, s_tok);
     }
-    float* q = reinterpret_cast<float*>(qa);
-    float* k = reinterpret_cast<float*>(ka);
-    float* v = reinterpret_cast<float*>(va);
+    const float* q = reinterpret_cast<const float*>(qa);
+    const float* k = reinterpret_cast<const float*>(ka);
+    const float* v = reinterpret_cast<const float*>(va);
     uint32_t mq = 0, mk = 0, mv = 0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      mq = max(mq, __float_as_uint(q[i]) & 0x7fffffffu);
-      mk = max(mk, __float_as_uint(k[i]) & 0x7fffffffu);
-      mv = max(mv, __float_as_uint(v[i]) & 0x7fffffffu);
+    for (int i = 0; i < DPT; ++i) {
+      mq = max(mq, qa[i] & 0x7fffffffu);
+      mk = max(mk, ka[i] & 0x7fffffffu);
+      mv = max(mv, va[i] & 0x7fffffffu);
     }
     mq = __reduce_max_sync(0xffffffffu, mq);
     mk = __reduce_max_sync(0xffffffffu, mk);
     mv = __reduce_max_sync(0xffffffffu, mv);
     if (ss) ss[1] = gtime();
-    compute_bar();  // rmax of the previous split has been read by everyone
+    compute_bar<CW>();  // rmax of the previous split has been read by everyone
     if (lane == 0) rmax[warp * 3] = mq, rmax[warp * 3 + 1] = mk, rmax[warp * 3 + 2] = mv;
     tc_fence_before();
-    compute_bar();  // also: every thread has read the accumulator and the scales
+    compute_bar<CW>();  // also: every thread has read the accumulator and the scales
     if (tid == 0) {
       if (!(trigger_late & 4)) mbar_arrive(accfree);
       mbar_arrive(&scfree[u & 1]);
     }
     {
-      const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
-                     cq = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+      const uint32_t a = lane < CW ? rmax[lane * 3] : 0u, bq = lane < CW ? rmax[lane * 3 + 1] : 0u,
+                     cq3 = lane < CW ? rmax[lane * 3 + 2] : 0u;
       mq = __reduce_max_sync(0xffffffffu, a);
       mk = __reduce_max_sync(0xffffffffu, bq);
-      mv = __reduce_max_sync(0xffffffffu, cq);
+      mv = __reduce_max_sync(0xffffffffu, cq3);
     }
     fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
     if (ss) ss[2] = gtime();
     {
-      uint32_t hi[16], lo[16];
+      uint32_t hi[DPT / 2], lo[DPT / 2];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
-      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 16 * half, hi);
-      tmem_st_32x32b_x16(tmem + lane_base + kT16Q + 32 + 16 * half, lo);
+      for (int j = 0; j < DPT / 2; ++j)
+        split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
+      tmem_st_cols<DPT / 2>(tmem + lane_base + kT16Q + (DPT / 2) * cq, hi);
+      tmem_st_cols<DPT / 2>(tmem + lane_base + kT16Q + 32 + (DPT / 2) * cq, lo);
     }
     {
-      uint32_t hi[16], lo[16];
+      uint32_t hi[DPT / 2], lo[DPT / 2];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
+      for (int j = 0; j < DPT / 2; ++j)
+        split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t off = row * 128 + ((((4 * half + c) ^ (row & 7))) << 4);
+      for (int c = 0; c < DPT / 8; ++c) {
+        const uint32_t off = row * 128 + (((((DPT / 8) * cq + c) ^ (row & 7))) << 4);
         *reinterpret_cast<uint4*>(sKh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
         *reinterpret_cast<uint4*>(sKl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
       }
@@ -1891,10 +1938,10 @@ __global__ void __launch_bounds__(kQaThreads, 1)
       if (ss) ss[3] = gtime();
       // V^T [64 dims][128 tokens] f16, 2 atoms of [64 x 128 B]: token t of dim d at
       // atom t / 64, row d, 16-byte chunk ((t % 64) / 8) ^ (d % 8), element t % 8.
-      // The even lane of a token pair writes dim kk, the odd lane dim 16 + (kk ^ 4)
-      // (their swizzled chunks differ: no bank conflict between the two halves).
-      // An element travels as one word, f16 hi | f16 lo << 16 (split_f16x2 of the
-      // dim pair, then byte permutes).
+      // Of this thread's DPT dims, the even lane of a token pair writes dim kk and
+      // the odd lane dim DPT/2 + (kk ^ 4) (their swizzled chunks differ: no bank
+      // conflict between the two halves).  An element travels as one word, f16 hi |
+      // f16 lo << 16 (split_f16x2 of the dim pair, then byte permutes).
       uint8_t* vh = sVT + vb * (2 * kH16);
       uint8_t* vl = vh + kH16;
       const bool odd = lane & 1;
@@ -1902,15 +1949,15 @@ __global__ void __launch_bounds__(kQaThreads, 1)
       const uint32_t tbase = (uint32_t)(t0 >> 6) * (64 * 128) + (uint32_t)(t0 & 7) * 2;
       const int tch = (t0 & 63) >> 3;
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const int dm = kk, dp = 16 + (kk ^ 4);
+      for (int kk = 0; kk < DPT / 2; ++kk) {
+        const int dm = kk, dp = DPT / 2 + (kk ^ 4);
         uint32_t hi2, lo2;  // (hi, lo) of dims dm (low halves) and dp (high halves)
         split_f16x2(__fmul_rn(v[dm], fv), __fmul_rn(v[dp], fv), hi2, lo2);
         const uint32_t e_dm = __byte_perm(hi2, lo2, 0x5410), e_dp = __byte_perm(hi2, lo2, 0x7632);
         const uint32_t recv = __shfl_xor_sync(0xffffffffu, odd ? e_dm : e_dp, 1);
         const uint32_t mine = odd ? e_dp : e_dm;
         const uint32_t ev = odd ? recv : mine, od = odd ? mine : recv;  // tokens t0, t0 + 1
-        const int d = 32 * half + (odd ? dp : dm);
+        const int d = DPT * cq + (odd ? dp : dm);
         const uint32_t off = tbase + (uint32_t)d * 128 + (uint32_t)((tch ^ (d & 7)) << 4);
         *reinterpret_cast<uint32_t*>(vh + off) = (ev & 0xffffu) | (od << 16);
         *reinterpret_cast<uint32_t*>(vl + off) = (ev >> 16) | (od & 0xffff0000u);
@@ -1920,7 +1967,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     tmem_st_wait();
     fence_proxy_async_smem();
     tc_fence_before();
-    compute_bar();
+    compute_bar<CW>();
     tc_fence_after();
     if (tid == 0) {
       if (trigger_late & 4) mbar_arrive(accfree);  // debug: GEMM after the whole split
@@ -1929,8 +1976,6 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     if (ss) ss[5] = gtime();
   };
 
-
-  // prologue: first unit's projection, split and S
   auto token_scale = [&](int hd) {
     const int grow = (hd / heads) * seq + row;
     return hd < nheads_total && grow < M ? __ldg(ts + grow) : 0.0f;
@@ -1953,71 +1998,74 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     if (ti) ti[0] = gtime();
     float oscale = 0.0f;
     if (cur) {
-    mbar_wait(barS, ph);
-    tc_fence_after();
-    if (ti) ti[1] = gtime();
-
-    // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
-    float s[64];
-    {
-      uint32_t r0[32], r1[32];
-      const uint32_t ta = tmem + lane_base + half * 64;
-      tmem_ld_32x32b_x32(ta, r0);
-      tmem_ld_32x32b_x32(ta + 32, r1);
-      tmem_ld_wait();
+      mbar_wait(barS, ph);
+      tc_fence_after();
+      if (ti) ti[1] = gtime();
+      // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
+      float s[KPT];
+      {
+        uint32_t r0[KPT];
+        tmem_ld_cols<KPT>(tmem + lane_base + KPT * cq, r0);
+        tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        s[j] = __uint_as_float(r0[j]);
-        s[32 + j] = __uint_as_float(r1[j]);
+        for (int j = 0; j < KPT; ++j) s[j] = __uint_as_float(r0[j]);
       }
-    }
-    float mx = -INFINITY;
-    if (seq == kAttT && !causal) {
+      float mx = -INFINITY;
+      if (seq == kAttT && !causal) {
 #pragma unroll
-      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
-    } else {
+        for (int j = 0; j < KPT; ++j) mx = fmaxf(mx, s[j]);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const int key = half * 64 + j;
-        if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
-        mx = fmaxf(mx, s[j]);
+        for (int j = 0; j < KPT; ++j) {
+          const int key = KPT * cq + j;
+          if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
+          mx = fmaxf(mx, s[j]);
+        }
       }
-    }
-    red[half * 128 + row] = mx;
-    compute_bar();
-    mx = fmaxf(red[row], red[128 + row]);
-    // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
-    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
-    const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
-    float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      redm[cq * 128 + row] = mx;
+      compute_bar<CW>();
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const float e = ex2_approx_f(__fmaf_rn(s[j], c, -mxc));
-      s[j] = e;
-      sp[j & 3] = __fadd_rn(sp[j & 3], e);
-    }
-    float sum = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
-    compute_bar();
-    red[half * 128 + row] = sum;
-    compute_bar();
-    sum = __fadd_rn(red[row], red[128 + row]);
-    // O = (P' V') / (fv sum'), sum' = 2^15 sum
-    oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
-    {
-      uint32_t hi[32], lo[32];
+      for (int c = 0; c < NCQ; ++c) mx = fmaxf(mx, redm[c * 128 + row]);
+      // exp(inv (s - max)) with s = S' / (fq fk): c = inv log2(e) / (fq fk), exact powers of two
+      const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
+      const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);  // P' = 2^15 exp(.): +15 in the exponent
+      // row sum in attention_f16_kernel's order: per 32-key quarter, four
+      // interleaved partials ((p0 + p1) + (p2 + p3)); quarters ((q0 + q1) + (q2 + q3))
+      float qs[KPT / 32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) split_f16x2(s[2 * j], s[2 * j + 1], hi[j], lo[j]);
-      tmem_st_32x32b_x32u(tmem + lane_base + 32 * half, hi);
-      tmem_st_32x32b_x32u(tmem + lane_base + 64 + 32 * half, lo);
+      for (int qq = 0; qq < KPT / 32; ++qq) {
+        float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = ex2_approx_f(__fmaf_rn(s[32 * qq + j], c, -mxc));
+          s[32 * qq + j] = e;
+          sp[j & 3] = __fadd_rn(sp[j & 3], e);
+        }
+        qs[qq] = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+      }
+      reds[cq * 128 + row] = KPT / 32 == 2 ? __fadd_rn(qs[0], qs[KPT / 32 - 1]) : qs[0];
+      compute_bar<CW>();
+      float sum;
+      if (NCQ == 2)
+        sum = __fadd_rn(reds[row], reds[128 + row]);
+      else
+        sum = __fadd_rn(__fadd_rn(reds[row], reds[128 + row]), __fadd_rn(reds[256 + row], reds[384 + row]));
+      // O = (P' V') / (fv sum'), sum' = 2^15 sum
+      oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
+      {
+        uint32_t hi[KPT / 2], lo[KPT / 2];
+#pragma unroll
+        for (int j = 0; j < KPT / 2; ++j) split_f16x2(s[2 * j], s[2 * j + 1], hi[j], lo[j]);
+        tmem_st_cols<KPT / 2>(tmem + lane_base + (KPT / 2) * cq, hi);
+        tmem_st_cols<KPT / 2>(tmem + lane_base + 64 + (KPT / 2) * cq, lo);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      compute_bar<CW>();
+      tc_fence_after();
+      if (ti) ti[2] = gtime();
+      if (tid == 0) mbar_arrive(prdy);  // O' = P' V' is issued by the attention MMA warp
     }
-    tmem_st_wait();
-    tc_fence_before();
-    compute_bar();
-    tc_fence_after();
-    if (ti) ti[2] = gtime();
-
-    if (tid == 0) mbar_arrive(prdy);  // O' = P' V' is issued by warp 10
-    }  // cur
     // ---- the next unit's projection epilogue and split run while the tensor
     //      core computes P V (the GEMM of the unit after streams meanwhile) ----
     if (nxt < nheads_total) {
@@ -2025,28 +2073,27 @@ __global__ void __launch_bounds__(kQaThreads, 1)
       if (ti) ti[4] = gtime();
       if (tr && !cur) tr[3] = gtime();
     }
-    if (cur) {
-      mbar_wait(barO, ph);
-      tc_fence_after();
-      if (ti) ti[5] = gtime();
-    }
     if (!cur) continue;
+    mbar_wait(barO, ph);
+    tc_fence_after();
+    if (ti) ti[5] = gtime();
     {
-      uint32_t r0[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + kT16O + half * 32, r0);
+      uint32_t r0[DPT];
+      tmem_ld_cols<DPT>(tmem + lane_base + kT16O + DPT * cq, r0);
       tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
+      for (int j = 0; j < DPT; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
       if (tma_store) {  // stage in this unit's V^T buffer (P V is done with it), SW128 f32 boxes
-        uint8_t* st = sVT + (it & 1) * (2 * kH16) + half * kH16 + row * 128;
+        const int col = DPT * cq;  // of the head's 64
+        uint8_t* st = sVT + (it & 1) * (2 * kH16) + (col >> 5) * kH16 + row * 128;
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          *reinterpret_cast<uint4*>(st + ((cc ^ (row & 7)) << 4)) =
-              make_uint4(r0[4 * cc], r0[4 * cc + 1], r0[4 * cc + 2], r0[4 * cc + 3]);
+        for (int c = 0; c < DPT / 4; ++c)
+          *reinterpret_cast<uint4*>(st + (((((col & 31) >> 2) + c) ^ (row & 7)) << 4)) =
+              make_uint4(r0[4 * c], r0[4 * c + 1], r0[4 * c + 2], r0[4 * c + 3]);
       } else if (row < seq) {
-        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + half * 32;
+        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + DPT * cq;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
+        for (int j = 0; j < DPT; j += 4)
           *reinterpret_cast<float4*>(dst + j) =
               make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
                           __uint_as_float(r0[j + 3]));
@@ -2054,7 +2101,7 @@ __global__ void __launch_bounds__(kQaThreads, 1)
     }
     if (tma_store) fence_proxy_async_smem();
     tc_fence_before();
-    compute_bar();  // O read out: the next P V may overwrite it
+    compute_bar<CW>();  // O read out: the next P V may overwrite it
     tc_fence_after();
     if (tma_store && tid == 0) {
       const uint8_t* st = sVT + (it & 1) * (2 * kH16);
@@ -2224,8 +2271,14 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   if (rc != ZQ_OK) return rc;
   static ZqDeviceOnce attr_once;
   attr_once([&](int) {
-    cudaFuncSetAttribute(qkv_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQaSmem);
+    cudaFuncSetAttribute(qkv_attention_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, QaCfg<8>::SMEM);
+    cudaFuncSetAttribute(qkv_attention_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, QaCfg<16>::SMEM);
   });
+  static int cw = -1;  // compute warps per CTA (ZQ_QA_CW = 8 | 16)
+  if (cw < 0) {
+    const char* ev = getenv("ZQ_QA_CW");
+    cw = ev && atoi(ev) == 8 ? 8 : 16;
+  }
   // seq == 128: whole 128-row boxes belong to one sequence, so O leaves by bulk TMA stores
   CUtensorMap tmc;
   int tma_store = 0;
@@ -2235,10 +2288,14 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   const int total = batch * heads;
   const int nsm = zq_num_sms();
   const int grid = total < nsm ? total : nsm;
-  cudaError_t e = launch_kernel(qkv_attention_kernel, dim3(grid), dim3(kQaThreads), kQaSmem,
-                                reinterpret_cast<cudaStream_t>(stream), 1, tmX, tmW, token_scales, w_row_scales, bias,
-                                (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx, total, g_att_trace, tmc,
-                                tma_store, qa_trigger_late());
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e =
+      cw == 8 ? launch_kernel(qkv_attention_kernel<8>, dim3(grid), dim3(QaCfg<8>::THREADS), QaCfg<8>::SMEM, st, 1, tmX,
+                              tmW, token_scales, w_row_scales, bias, (int)M, seq, heads, dmodel, causal, scale, ctx,
+                              ld_ctx, total, g_att_trace, tmc, tma_store, qa_trigger_late())
+              : launch_kernel(qkv_attention_kernel<16>, dim3(grid), dim3(QaCfg<16>::THREADS), QaCfg<16>::SMEM, st, 1,
+                              tmX, tmW, token_scales, w_row_scales, bias, (int)M, seq, heads, dmodel, causal, scale,
+                              ctx, ld_ctx, total, g_att_trace, tmc, tma_store, qa_trigger_late());
   if (e != cudaSuccess) {
     set_error("fused QKV attention launch: %s", cudaGetErrorString(e));
     return ZQ_ERR_CUDA;
