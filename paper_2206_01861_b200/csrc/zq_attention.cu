@@ -2116,6 +2116,484 @@ __global__ void __launch_bounds__(QaCfg<CW>::THREADS, 1)
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Split-role variant of the fused kernel (16 compute warps): warps 8-15 dequantize
+// and split unit u + 1 while warps 0-7 run unit u's softmax and O, so the two
+// CUDA-core phases overlap instead of taking turns on the same warps.  Scales per
+// unit travel through smem (sfr), the V^T buffer is handed back by the attention
+// warps once O has been staged out of it (vtfree).  Same arithmetic and order as
+// qkv_attention_kernel: ctx is bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int kQsThreads = 640;
+constexpr int kQsSmem = kQaX + 6 * kH16 + kQaSc + 168 + 8 * 3 * 4 + 4 * 128 * 4 + 32;
+
+__global__ void __launch_bounds__(kQsThreads, 1)
+    qkv_attention_split_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                         const float* __restrict__ ts, const float* __restrict__ rs, const float* __restrict__ bias,
+                         int M, int seq, int heads, int dmodel, int causal, float scale, float* __restrict__ ctx,
+                         int64_t ld_ctx, int nheads_total, unsigned long long* __restrict__ trace,
+                         const __grid_constant__ CUtensorMap tmc, int tma_store, int trigger_late) {
+  constexpr int KPT = 64, DPT = 32;  // 8 attention + 8 convert warps, 2 column halves per row
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sX = sm;
+  uint8_t* sKh = sm + kQaX;
+  uint8_t* sKl = sKh + kH16;
+  uint8_t* sVT = sKl + kH16;  // [2 buffers][hi | lo]
+  float* sSc = reinterpret_cast<float*>(sVT + 4 * kH16);  // per-unit weight scales and bias
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVT + 4 * kH16 + kQaSc);
+  uint64_t* gfull = bars;       // [3] operand stage landed
+  uint64_t* gempty = bars + 3;  // [3] operand stage consumed by the MMAs
+  uint64_t* accf = bars + 6;    // GEMM accumulator complete
+  uint64_t* accfree = bars + 7; // accumulator read by the epilogue
+  uint64_t* barS = bars + 8;
+  uint64_t* barO = bars + 9;
+  uint64_t* scf = bars + 10;    // [2] unit parity: scales and bias landed
+  uint64_t* scfree = bars + 12; // [2] unit parity: scales and bias read by epi_split
+  uint64_t* qkr = bars + 14;    // Q, K, V^T of the next unit split (S may be issued)
+  uint64_t* prdy = bars + 15;   // P written (P V may be issued)
+  // per unit parity (a single barrier could complete twice before the convert
+  // warps look: the attention warps may finish units u - 2 and u - 1 first)
+  uint64_t* vtfree = bars + 16; // [2] O of unit u staged out of V^T buffer u & 1
+  uint64_t* sfr = bars + 18;    // [2] unit parity: the unit's power-of-two scales written
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(bars + 21);  // [8 convert warps][3]
+  float* redm = reinterpret_cast<float*>(rmax + 8 * 3);     // [2][128] row partial maxima
+  float* reds = redm + 2 * 128;                             // [2][128] row partial sums
+  float* sfs = reds + 2 * 128;                              // [2][4] (fq, fk, fv) per unit parity
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkb = dmodel / 128;
+  if (tid == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+    for (int i = 0; i < 20; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
+  if (tr) tr[0] = gtime();
+  // PDL: dependents may launch only once every warp has resized its registers (a
+  // dependent CTA landing on this SM could otherwise take the registers the TMA /
+  // MMA warpgroup released before the convert warps claim them: deadlock)
+  auto resized = [&]() {
+    asm volatile("bar.sync 3, %0;" ::"n"(kQsThreads) : "memory");
+    if (!(trigger_late & 1)) pdl_trigger();
+  };
+  // registers: the 640 threads launch at 96 each (61440, the CTA's pool); the TMA /
+  // MMA warpgroup gives 48 of its 96 to the convert warps (dequant + split hold 3 x
+  // 32 values): 4 x 48 + 8 x 96 + 8 x 120 = 20 x 96.  setmaxnreg.inc only draws on
+  // what the CTA's own dec released.  Each role's code sits inside the branch that
+  // resizes its warpgroup.
+  if (warp >= 16) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    resized();
+
+  if (warp == 16) {  // ===== GEMM operand producer =====
+    if (lane == 0) {
+      // the unit's 192 weight-row scales and biases -> buffer u & 1 (free once
+      // epi_split(u - 2) has read it)
+      auto load_scales = [&](int h, int u) {
+        if (u >= 2) mbar_wait_idle(&scfree[u & 1], ((u >> 1) - 1) & 1);
+        float* dst = sSc + (u & 1) * (2 * 3 * kAttD);
+        mbar_arrive_expect_tx(&scf[u & 1], (bias ? 2 : 1) * 3 * kAttD * 4);
+#pragma unroll
+        for (int part = 0; part < 3; ++part) {
+          bulk_load_1d(dst + part * kAttD, rs + part * dmodel + h * kAttD, kAttD * 4, &scf[u & 1]);
+          if (bias) bulk_load_1d(dst + 3 * kAttD + part * kAttD, bias + part * dmodel + h * kAttD, kAttD * 4,
+                                 &scf[u & 1]);
+        }
+      };
+      auto load_w = [&](uint8_t* st, int kb, int h, uint64_t* bar) {
+#pragma unroll
+        for (int part = 0; part < 3; ++part)
+          tma_load_2d(st + kQaStageA + part * (kAttD * 128), &tmW, bar, kb * 128, part * dmodel + h * kAttD);
+      };
+      // weights and scales do not depend on the previous kernel: unit 0's first
+      // stages of B go out before griddepcontrol.wait, A (the activations) after it
+      const int npre = nkb < kQaStages ? nkb : kQaStages;
+      if ((int)blockIdx.x < nheads_total) {
+        const int h0 = (int)blockIdx.x % heads;
+        load_scales(h0, 0);
+        for (int kb = 0; kb < npre; ++kb) {
+          mbar_arrive_expect_tx(&gfull[kb], kQaStage);
+          load_w(sX + kb * kQaStage, kb, h0, &gfull[kb]);
+        }
+      }
+      pdl_wait();
+      if (tr) tr[1] = gtime();
+      int kc = 0, u = 0;
+      for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
+        const int b = hd / heads, h = hd % heads;
+        if ((trigger_late & 2) && u >= 1) mbar_wait(accfree, (u - 1) & 1);  // debug: no operand prefetch
+        if (u > 0) load_scales(h, u);
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const int s = kc % kQaStages;
+          uint8_t* st = sX + s * kQaStage;
+          if (u == 0 && kb < npre) {  // B already in flight
+            tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
+            continue;
+          }
+          if (kc >= kQaStages) mbar_wait_idle(&gempty[s], ((kc / kQaStages) - 1) & 1);
+          if (trace && kb == 0 && kc / nkb < 4) trace[(size_t)blockIdx.x * 64 + 60 + kc / nkb] = gtime();
+          mbar_arrive_expect_tx(&gfull[s], kQaStage);
+          tma_load_2d(st, &tmX, &gfull[s], kb * 128, b * seq);
+          load_w(st, kb, h, &gfull[s]);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 17) {  // ===== GEMM MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_i8(128, 3 * kAttD);
+      int kc = 0, u = 0;
+      for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
+        if (u > 0) mbar_wait_idle(accfree, (u - 1) & 1);  // the previous unit's accumulator has been read
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const int s = kc % kQaStages;
+          mbar_wait(&gfull[s], (kc / kQaStages) & 1);
+          tc_fence_after();
+          if (trace && kb == nkb - 1 && u < 4) trace[(size_t)blockIdx.x * 64 + 56 + u] = gtime();
+          if (trace && kb == 0 && u < 4) trace[(size_t)blockIdx.x * 64 + 52 + u] = gtime();
+          const uint32_t a_addr = smem_u32(sX + s * kQaStage);
+          const uint32_t b_addr = a_addr + kQaStageA;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_i8(tmem + kQaAcc, make_sw128_desc(a_addr + k * 32), make_sw128_desc(b_addr + k * 32), idesc,
+                   (kb | k) != 0);
+          mma_commit(&gempty[s]);
+        }
+        mma_commit(accf);
+      }
+    }
+    return;
+  }
+
+  if (warp == 18) {  // ===== attention MMA issuer: S = Q K^T, O = P V (3-term f16 splits) =====
+    int it = 0;
+    for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+      mbar_wait_idle(qkr, it & 1);                         // Q, K, V^T of unit it split
+      if (it > 0) mbar_wait_idle(barO, (it - 1) & 1);      // P of unit it - 1 consumed
+      tc_fence_after();
+      {
+        const uint32_t idesc = make_idesc_f16(128, 128);
+        const uint64_t dKh = make_sw128_desc(smem_u32(sKh)), dKl = make_sw128_desc(smem_u32(sKl));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttD / 16; ++ks)
+            mma_f16_ts_elect(tmem, tmem + kT16Q + (t3 == 2 ? 32 : 0) + 8 * ks, (t3 == 1 ? dKl : dKh) + 2 * ks,
+                             idesc, (t3 | ks) != 0);
+        mma_commit_elect(barS);
+      }
+      mbar_wait_idle(prdy, it & 1);                        // P of unit it written
+      tc_fence_after();
+      {
+        const uint32_t idesc = make_idesc_f16(128, kAttD);
+        const uint8_t* vh = sVT + (it & 1) * (2 * kH16);
+        const uint64_t dVh = make_sw128_desc(smem_u32(vh)), dVl = make_sw128_desc(smem_u32(vh + kH16));
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int ks = 0; ks < kAttT / 16; ++ks) {
+            const uint64_t boff = (uint64_t)(((ks >> 2) * (64 * 128) + (ks & 3) * 32) >> 4);
+            mma_f16_ts_elect(tmem + kT16O, tmem + (t3 == 2 ? 64 : 0) + 8 * ks, (t3 == 1 ? dVl : dVh) + boff, idesc,
+                             (t3 | ks) != 0);
+          }
+        mma_commit_elect(barO);
+      }
+    }
+    return;
+  }
+
+    return;  // warp 19
+  }
+  const int quarter = warp & 3, half = (warp >> 2) & 1;  // TMEM lane quarter, column half
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+  auto token_scale = [&](int hd) {
+    const int grow = (hd / heads) * seq + row;
+    return hd < nheads_total && grow < M ? __ldg(ts + grow) : 0.0f;
+  };
+
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 120;" ::: "memory");
+    resized();
+    pdl_wait();  // token scales come from the previous kernel
+    // ===== convert warps 8-15: accumulator of unit u -> Q hi/lo (TMEM), K hi/lo and
+    //       V^T hi/lo (smem), the next split overlapping the attention warps' softmax =====
+    const int gtid = tid - 256;  // 0 .. 255
+    unsigned long long* trb = (trace && gtid == 0) ? trace + (size_t)blockIdx.x * 64 : nullptr;
+    auto gbar = []() { asm volatile("bar.sync 2, 256;" ::: "memory"); };
+    auto dequant = [&](uint32_t* r, const float* sw, const float* sb, bool live, float s_tok) {
+#pragma unroll
+      for (int j = 0; j < DPT / 4; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(sw + 4 * j);
+        r[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x));
+        r[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y));
+        r[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z));
+        r[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w));
+      }
+      if (bias != nullptr) {
+#pragma unroll
+        for (int j = 0; j < DPT / 4; ++j) {
+          const float4 bb = *reinterpret_cast<const float4*>(sb + 4 * j);
+          r[4 * j + 0] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 0]), bb.x));
+          r[4 * j + 1] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 1]), bb.y));
+          r[4 * j + 2] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 2]), bb.z));
+          r[4 * j + 3] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * j + 3]), bb.w));
+        }
+      }
+      if (!live) {
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) r[j] = 0u;
+      }
+    };
+    int u = 0;
+    float s_tok = token_scale(blockIdx.x);
+    for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++u) {
+      const int vb = u & 1;
+      const bool live = (hd / heads) * seq + row < M;
+      const float s_tok_next = token_scale(hd + (int)gridDim.x);
+      unsigned long long* st_acc = trb ? (u == 0 ? trb + 2 : u <= 6 ? trb + 8 + (u - 1) * 8 + 3 : nullptr) : nullptr;
+      uint32_t qa[DPT], ka[DPT], va[DPT];
+      mbar_wait(accf, u & 1);
+      tc_fence_after();
+      if (st_acc) *st_acc = gtime();
+      tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + DPT * half, qa);
+      tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + kAttD + DPT * half, ka);
+      tmem_ld_cols<DPT>(tmem + lane_base + kQaAcc + 2 * kAttD + DPT * half, va);
+      mbar_wait(&scf[u & 1], (u >> 1) & 1);
+      tmem_ld_wait();
+      {
+        const float* sw = sSc + (u & 1) * (2 * 3 * kAttD) + DPT * half;
+        dequant(qa, sw, sw + 3 * kAttD, live, s_tok);
+        dequant(ka, sw + kAttD, sw + 4 * kAttD, live, s_tok);
+        dequant(va, sw + 2 * kAttD, sw + 5 * kAttD, live, s_tok);
+      }
+      uint32_t mq = 0, mk = 0, mv = 0;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) {
+        mq = max(mq, qa[i] & 0x7fffffffu);
+        mk = max(mk, ka[i] & 0x7fffffffu);
+        mv = max(mv, va[i] & 0x7fffffffu);
+      }
+      mq = __reduce_max_sync(0xffffffffu, mq);
+      mk = __reduce_max_sync(0xffffffffu, mk);
+      mv = __reduce_max_sync(0xffffffffu, mv);
+      gbar();  // rmax of the previous split has been read by everyone
+      if (lane == 0) rmax[(warp - 8) * 3] = mq, rmax[(warp - 8) * 3 + 1] = mk, rmax[(warp - 8) * 3 + 2] = mv;
+      tc_fence_before();
+      gbar();  // also: every thread has read the accumulator and the scales
+      if (gtid == 0) {
+        if (!(trigger_late & 4)) mbar_arrive(accfree);
+        mbar_arrive(&scfree[u & 1]);
+      }
+      {
+        const uint32_t a = lane < 8 ? rmax[lane * 3] : 0u, bq = lane < 8 ? rmax[lane * 3 + 1] : 0u,
+                       cq3 = lane < 8 ? rmax[lane * 3 + 2] : 0u;
+        mq = __reduce_max_sync(0xffffffffu, a);
+        mk = __reduce_max_sync(0xffffffffu, bq);
+        mv = __reduce_max_sync(0xffffffffu, cq3);
+      }
+      const float fq = pow2_scale_for(mq), fk = pow2_scale_for(mk), fv = pow2_scale_for(mv);
+      const float* q = reinterpret_cast<const float*>(qa);
+      const float* k = reinterpret_cast<const float*>(ka);
+      const float* v = reinterpret_cast<const float*>(va);
+      if (u >= 1) {  // S of the previous unit has read Q and K
+        mbar_wait(barS, (u - 1) & 1);
+        tc_fence_after();
+      }
+      {
+        uint32_t hi[DPT / 2], lo[DPT / 2];
+#pragma unroll
+        for (int j = 0; j < DPT / 2; ++j)
+          split_f16x2(__fmul_rn(q[2 * j], fq), __fmul_rn(q[2 * j + 1], fq), hi[j], lo[j]);
+        tmem_st_cols<DPT / 2>(tmem + lane_base + kT16Q + (DPT / 2) * half, hi);
+        tmem_st_cols<DPT / 2>(tmem + lane_base + kT16Q + 32 + (DPT / 2) * half, lo);
+      }
+      {
+        uint32_t hi[DPT / 2], lo[DPT / 2];
+#pragma unroll
+        for (int j = 0; j < DPT / 2; ++j)
+          split_f16x2(__fmul_rn(k[2 * j], fk), __fmul_rn(k[2 * j + 1], fk), hi[j], lo[j]);
+#pragma unroll
+        for (int c = 0; c < DPT / 8; ++c) {
+          const uint32_t off = row * 128 + (((((DPT / 8) * half + c) ^ (row & 7))) << 4);
+          *reinterpret_cast<uint4*>(sKh + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+          *reinterpret_cast<uint4*>(sKl + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+        }
+      }
+      if (u >= 2) mbar_wait(&vtfree[vb], ((u >> 1) - 1) & 1);  // O of unit u - 2 has left V^T buffer vb
+      {
+        // V^T as in qkv_attention_kernel: token pairs across adjacent lanes, the even
+        // lane writes dim kk, the odd lane DPT/2 + (kk ^ 4)
+        uint8_t* vh = sVT + vb * (2 * kH16);
+        uint8_t* vl = vh + kH16;
+        const bool odd = lane & 1;
+        const int t0 = row & ~1;
+        const uint32_t tbase = (uint32_t)(t0 >> 6) * (64 * 128) + (uint32_t)(t0 & 7) * 2;
+        const int tch = (t0 & 63) >> 3;
+#pragma unroll
+        for (int kk = 0; kk < DPT / 2; ++kk) {
+          const int dm = kk, dp = DPT / 2 + (kk ^ 4);
+          uint32_t hi2, lo2;
+          split_f16x2(__fmul_rn(v[dm], fv), __fmul_rn(v[dp], fv), hi2, lo2);
+          const uint32_t e_dm = __byte_perm(hi2, lo2, 0x5410), e_dp = __byte_perm(hi2, lo2, 0x7632);
+          const uint32_t recv = __shfl_xor_sync(0xffffffffu, odd ? e_dm : e_dp, 1);
+          const uint32_t mine = odd ? e_dp : e_dm;
+          const uint32_t ev = odd ? recv : mine, od = odd ? mine : recv;
+          const int d = DPT * half + (odd ? dp : dm);
+          const uint32_t off = tbase + (uint32_t)d * 128 + (uint32_t)((tch ^ (d & 7)) << 4);
+          *reinterpret_cast<uint32_t*>(vh + off) = (ev & 0xffffu) | (od << 16);
+          *reinterpret_cast<uint32_t*>(vl + off) = (ev >> 16) | (od & 0xffff0000u);
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      gbar();
+      tc_fence_after();
+      if (gtid == 0) {
+        if (trigger_late & 4) mbar_arrive(accfree);
+        // the attention warps take this unit's scales from a slot per unit parity
+        // (free: the attention warps read unit u - 2's before their O of u - 2,
+        // which this split waited for through vtfree)
+        sfs[4 * (u & 1)] = fq, sfs[4 * (u & 1) + 1] = fk, sfs[4 * (u & 1) + 2] = fv;
+        mbar_arrive(&sfr[u & 1]);
+        mbar_arrive(qkr);  // S of unit u may be issued
+      }
+      if (trb && u <= 6) {
+        if (u == 0) trb[3] = gtime();
+        else trb[8 + (u - 1) * 8 + 4] = gtime();
+      }
+      s_tok = s_tok_next;
+    }
+    return;
+  }
+  // ===== attention warps 0-7: softmax of unit it (P into TMEM), then its O =====
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");
+  resized();
+  pdl_wait();
+  auto abar = []() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+  int it = 0;
+  for (int hd = blockIdx.x; hd < nheads_total; hd += gridDim.x, ++it) {
+    const uint32_t ph = it & 1;
+    const int b = hd / heads, h = hd % heads;
+    unsigned long long* ti = (tr && it < 6) ? tr + 8 + it * 8 : nullptr;
+    if (ti) ti[0] = gtime();
+    mbar_wait(barS, ph);
+    tc_fence_after();
+    mbar_wait(&sfr[it & 1], (it >> 1) & 1);
+    const float cfq = sfs[4 * (it & 1)], cfk = sfs[4 * (it & 1) + 1], cfv = sfs[4 * (it & 1) + 2];
+    if (ti) ti[1] = gtime();
+    // ---- softmax: S' from TMEM; P' = 2^15 exp(.) as f16 hi / lo back into TMEM ----
+    float s[KPT];
+    {
+      uint32_t r0[KPT];
+      tmem_ld_cols<KPT>(tmem + lane_base + KPT * half, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) s[j] = __uint_as_float(r0[j]);
+    }
+    float mx = -INFINITY;
+    if (seq == kAttT && !causal) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) mx = fmaxf(mx, s[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int key = KPT * half + j;
+        if (key >= seq || (causal && key > row)) s[j] = -INFINITY;  // mask (transformer.py:433-434)
+        mx = fmaxf(mx, s[j]);
+      }
+    }
+    redm[half * 128 + row] = mx;
+    abar();
+    mx = fmaxf(redm[row], redm[128 + row]);
+    const float c = __fmul_rn(__fmul_rn(__fmul_rn(scale, 1.4426950408889634f), pow2_inv(cfq)), pow2_inv(cfk));
+    const float mxc = __fsub_rn(__fmul_rn(mx, c), 15.0f);
+    float qs[2];
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq) {
+      float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = ex2_approx_f(__fmaf_rn(s[32 * qq + j], c, -mxc));
+        s[32 * qq + j] = e;
+        sp[j & 3] = __fadd_rn(sp[j & 3], e);
+      }
+      qs[qq] = __fadd_rn(__fadd_rn(sp[0], sp[1]), __fadd_rn(sp[2], sp[3]));
+    }
+    reds[half * 128 + row] = __fadd_rn(qs[0], qs[1]);
+    abar();
+    const float sum = __fadd_rn(reds[row], reds[128 + row]);
+    const float oscale = __fmul_rn(__frcp_rn(sum), pow2_inv(cfv));
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {  // P hi / lo in two 16-word halves (registers)
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_f16x2(s[32 * hh + 2 * j], s[32 * hh + 2 * j + 1], hi[j], lo[j]);
+      tmem_st_cols<16>(tmem + lane_base + (KPT / 2) * half + 16 * hh, hi);
+      tmem_st_cols<16>(tmem + lane_base + 64 + (KPT / 2) * half + 16 * hh, lo);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    abar();
+    tc_fence_after();
+    if (ti) ti[2] = gtime();
+    if (tid == 0) mbar_arrive(prdy);  // O' = P' V' is issued by the attention MMA warp
+    mbar_wait(barO, ph);
+    tc_fence_after();
+    if (ti) ti[5] = gtime();
+    {
+      uint32_t r0[DPT];
+      tmem_ld_cols<DPT>(tmem + lane_base + kT16O + DPT * half, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) r0[j] = __float_as_uint(__fmul_rn(__uint_as_float(r0[j]), oscale));
+      if (tma_store) {  // stage in this unit's V^T buffer (P V is done with it), SW128 f32 boxes
+        uint8_t* st = sVT + (it & 1) * (2 * kH16) + half * kH16 + row * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<uint4*>(st + ((cc ^ (row & 7)) << 4)) =
+              make_uint4(r0[4 * cc], r0[4 * cc + 1], r0[4 * cc + 2], r0[4 * cc + 3]);
+      } else if (row < seq) {
+        float* dst = ctx + ((int64_t)b * seq + row) * ld_ctx + h * kAttD + DPT * half;
+#pragma unroll
+        for (int j = 0; j < DPT; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
+                          __uint_as_float(r0[j + 3]));
+      }
+    }
+    if (tma_store) fence_proxy_async_smem();
+    tc_fence_before();
+    abar();  // O read out: the next P V may overwrite it
+    tc_fence_after();
+    if (tid == 0) {
+      if (tma_store) {
+        const uint8_t* st = sVT + (it & 1) * (2 * kH16);
+        tma_store_2d(&tmc, st, h * kAttD, b * seq);
+        tma_store_2d(&tmc, st + kH16, h * kAttD + 32, b * seq);
+        bulk_commit();
+        bulk_wait_read0();  // the staging (V^T buffer it & 1) has been read
+      }
+      mbar_arrive(&vtfree[it & 1]);
+    }
+    if (ti) ti[6] = gtime();
+  }
+  if (tma_store && tid == 0) bulk_wait0();
+  if (trigger_late & 1) pdl_trigger();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 int make_tmap_f32(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld_bytes,
                   int box_cols, int box_rows, CUtensorMapSwizzle sw);
 int make_tmap_2d(CUtensorMap* tm, CUtensorMapDataType dt, const void* base, int64_t rows, int64_t cols,
@@ -2273,11 +2751,17 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   attr_once([&](int) {
     cudaFuncSetAttribute(qkv_attention_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, QaCfg<8>::SMEM);
     cudaFuncSetAttribute(qkv_attention_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, QaCfg<16>::SMEM);
+    cudaFuncSetAttribute(qkv_attention_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQsSmem);
   });
-  static int cw = -1;  // compute warps per CTA (ZQ_QA_CW = 8 | 16)
+  // variant (ZQ_QA_CW): 16 (default) / 8 compute warps taking turns on split and
+  // softmax, or 0 = split roles (8 convert + 8 attention warps, setmaxnreg): in the
+  // BERT graph 22.2 / 24.4 / 21.9 us per layer — the split roles gain little (the two
+  // groups compete for the same schedulers), so the simpler kernel is the default
+  static int cw = -1;
   if (cw < 0) {
     const char* ev = getenv("ZQ_QA_CW");
-    cw = ev && atoi(ev) == 8 ? 8 : 16;
+    cw = ev ? atoi(ev) : 16;
+    if (cw != 8 && cw != 0) cw = 16;
   }
   // seq == 128: whole 128-row boxes belong to one sequence, so O leaves by bulk TMA stores
   CUtensorMap tmc;
@@ -2290,7 +2774,10 @@ extern "C" int zq_qkv_attention(const int8_t* xq, int64_t ld_x, const float* tok
   const int grid = total < nsm ? total : nsm;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e =
-      cw == 8 ? launch_kernel(qkv_attention_kernel<8>, dim3(grid), dim3(QaCfg<8>::THREADS), QaCfg<8>::SMEM, st, 1, tmX,
+      cw == 0 ? launch_kernel(qkv_attention_split_kernel, dim3(grid), dim3(kQsThreads), kQsSmem, st, 1, tmX, tmW,
+                              token_scales, w_row_scales, bias, (int)M, seq, heads, dmodel, causal, scale, ctx, ld_ctx,
+                              total, g_att_trace, tmc, tma_store, qa_trigger_late())
+      : cw == 8 ? launch_kernel(qkv_attention_kernel<8>, dim3(grid), dim3(QaCfg<8>::THREADS), QaCfg<8>::SMEM, st, 1, tmX,
                               tmW, token_scales, w_row_scales, bias, (int)M, seq, heads, dmodel, causal, scale, ctx,
                               ld_ctx, total, g_att_trace, tmc, tma_store, qa_trigger_late())
               : launch_kernel(qkv_attention_kernel<16>, dim3(grid), dim3(QaCfg<16>::THREADS), QaCfg<16>::SMEM, st, 1,
