@@ -119,3 +119,37 @@ def test_engine_fused_qkv_bit_identical(zq, causal):
         eng.check_finite()
         assert eng._fuse_qkv == fuse  # the fused shape was accepted
     assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
+
+
+_VARIANT_CHECK = r"""
+import math, sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import test_qkv_attention_gpu as Tq
+from paper_2206_01861_b200 import _native as N, quant
+for batch, seq, heads, causal in ((32, 128, 12, False), (5, 100, 12, False), (7, 128, 4, True)):
+    xq, w, bias = Tq._case(quant, batch, seq, 64 * heads, 48 if heads == 12 else 8, seed=batch + seq)
+    ref = Tq._unfused(N, xq, w, bias, batch, seq, heads, causal)
+    rc, out = Tq._fused(N, xq, w, bias, batch, seq, heads, causal)
+    assert rc == N.ZQ_OK and torch.equal(out.view(torch.int32), ref.view(torch.int32)), (batch, seq, heads)
+    for _ in range(3):  # back-to-back launches (programmatic dependent launch between them)
+        Tq._fused(N, xq, w, bias, batch, seq, heads, causal)
+    torch.cuda.synchronize()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("variant", ["8", "0"])
+def test_fused_qkv_attention_variants(variant):
+    """The selectable kernel variants (ZQ_QA_CW=8: 8 compute warps; 0: split
+    convert / attention roles) are bit-identical too; the variant is chosen once
+    per process, so each runs in its own interpreter (timeout: a hang fails)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _VARIANT_CHECK.format(root=root, tests=os.path.join(root, "tests"))
+    env = dict(os.environ, ZQ_QA_CW=variant)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
