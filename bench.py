@@ -490,17 +490,31 @@ def run_ours(args, rank: int, world: int, dist):
     eng.check_finite()
 
     # ---- end to end through the public API with host buffers ----
-    # Every step: pinned-host ids H2D (inside forward()), the forward, and a D2H of
-    # the step's hidden states.  The D2H of step i runs on a copy stream from a
-    # device snapshot while step i+1 computes (the serving pipeline): it is issued
-    # once step i+1's L2 flush has finished, so it overlaps the forward rather
-    # than the flush (whose own time is subtracted); the timed region spans all
-    # steps and ends when the last D2H has landed.
+    # Every step: an H2D of the step's token ids from pinned host memory, the
+    # forward (EncoderEngine.forward), and a D2H of the step's hidden states.  As
+    # in a serving pipeline, step i+1's ids travel on an upload stream while step
+    # i computes (forward() then takes them device to device), and the D2H of step
+    # i runs on a copy stream from a device snapshot while step i+1 computes: it is
+    # issued once step i+1's L2 flush has finished, so it overlaps the forward
+    # rather than the flush (whose own time is subtracted); the timed region spans
+    # all steps, from the first upload to the last D2H.
     out_host = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32).pin_memory() for _ in range(2)]
     snap = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32, device="cuda") for _ in range(2)]
     copy_stream = torch.cuda.Stream()
+    up_stream = torch.cuda.Stream()
+    ids_dev = [torch.empty_like(ids_host, device="cuda") for _ in range(2)]
+    uploaded = [None, None]
+    consumed = [None, None]
     copied = [None, None]
     pending = None  # (slot, ready event) of the step whose D2H is still to be issued
+
+    def upload(slot):
+        if consumed[slot] is not None:
+            up_stream.wait_event(consumed[slot])  # the forward that read this slot has copied it
+        with torch.cuda.stream(up_stream):
+            ids_dev[slot].copy_(ids_host, non_blocking=True)  # H2D of a step's ids
+        uploaded[slot] = torch.cuda.Event()
+        uploaded[slot].record(up_stream)
 
     def issue_d2h(slot, ready):
         copy_stream.wait_event(ready)
@@ -513,6 +527,8 @@ def run_ours(args, rank: int, world: int, dist):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush_ev = []
     a.record(stream)
+    up_stream.wait_event(a)
+    upload(0)
     for i in range(args.steps):
         fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         fa.record(stream)
@@ -522,8 +538,13 @@ def run_ours(args, rank: int, world: int, dist):
         if pending is not None:              # previous step's D2H, after this flush
             copy_stream.wait_event(fb)
             issue_d2h(*pending)
-        out = eng.forward(ids_host)          # H2D of ids inside
         j = i % 2
+        stream.wait_event(uploaded[j])
+        out = eng.forward(ids_dev[j])        # ids device to device, then the forward graph
+        consumed[j] = torch.cuda.Event()
+        consumed[j].record(stream)
+        if i + 1 < args.steps:
+            upload((i + 1) % 2)              # the next step's ids, during this forward
         if copied[j] is not None:
             stream.wait_event(copied[j])     # the D2H that read snap[j] is done
         snap[j].copy_(out)
