@@ -127,3 +127,33 @@ def test_scale_double_rounding_equals_f32_division():
         ref = (a.astype(np.float64) / qm).astype(np.float32)
         dev = a / np.float32(qm)
         assert np.array_equal(ref.view(np.uint32), dev.view(np.uint32)), qm
+
+
+def test_no_global_load_scheduled_before_the_grid_dependency_wait():
+    """Programmatic dependent launch: a kernel may start while its predecessor
+    still runs, so reads of the predecessor's output must come after
+    griddepcontrol.wait (SASS ACQBULK).  ptxas treats non-coherent loads as
+    invariant and once scheduled two of tok_quant_kernel<16, 256>'s row loads
+    above the wait: scan every kernel of the built library for an LDG before its
+    first ACQBULK.  Allowed: decode attention's lens[b] (written by a non-PDL
+    torch op at the start of the step, before any kernel of the step)."""
+    import shutil
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_2206_01861_b200", "libzq_b200.so")
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(lib) or not os.path.exists(cuobjdump):
+        pytest.skip("library or cuobjdump not available")
+    sass = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True, check=True).stdout
+    offenders = []
+    name, seen_wait, early = None, False, 0
+    for line in sass.splitlines() + ["Function : <end>"]:
+        if "Function :" in line:
+            if name and seen_wait and early and "decode_attention_tma_kernel" not in name:
+                offenders.append((name, early))
+            name, seen_wait, early = line.split("Function :")[1].strip(), False, 0
+        elif "ACQBULK" in line:
+            seen_wait = True
+        elif re.search(r"\sLDG\.E", line) and not seen_wait:
+            early += 1
+    assert not offenders, offenders
