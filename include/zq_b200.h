@@ -306,13 +306,19 @@ int zq_gelu_estimate(const float* x, int64_t n, float* est, float* bound, void* 
  * epilogue start / end, 63 epilogue exit).  Not thread-safe; tooling only. */
 int zq_gemm_set_trace(unsigned long long* buf);
 
-/* Diagnostics: mode 20 makes zq_attention_f32 record 8 %globaltimer stamps per
- * CTA (phase boundaries) into ctx instead of its output; 0 = normal. */
+/* Kept for ABI stability: mode 0 returns ZQ_OK, any other mode
+ * ZQ_ERR_UNSUPPORTED (the phase timeline moved to zq_attention_set_trace). */
 int zq_attention_debug(int mode);
 
-/* Diagnostics: when buf != NULL, the short-sequence attention kernel records
- * %globaltimer stamps buf[cta*64 + head_iter*8 + phase] (phase 0 loop start,
- * 1 operands landed, 2 split done, 3 S done, 4 P in TMEM, 5 O done, 6 stored). */
+/* Diagnostics: when buf != NULL (148 x 64 u64), the attention kernels launched
+ * afterwards record %globaltimer stamps per CTA: attention_f16_kernel at
+ * buf[cta*64 + head_iter*8 + phase] (phase 0 loop start, 1 operands landed,
+ * 2 split done, 3 S done, 4 P in TMEM, 5 O done, 6 stored); the fused QKV +
+ * attention kernel at buf[cta*64 + 8 + unit*8 + phase] (0 start, 1 S ready,
+ * 2 P written, 3 next accumulator ready, 4 next split done, 5 P V done, 6 end,
+ * 7 loop top), its prologue at [2], [3] and the GEMM warps at [52..63]
+ * (tools/qa_trace.py reads them).  The pointer is a launch argument, so a
+ * captured graph keeps the one set at capture. */
 int zq_attention_set_trace(unsigned long long* buf);
 
 
