@@ -494,12 +494,24 @@ def run_ours(args, rank: int, world: int, dist):
     # forward (EncoderEngine.forward), and a D2H of the step's hidden states.  As
     # in a serving pipeline, step i+1's ids travel on an upload stream while step
     # i computes (forward() then takes them device to device), and the D2H of step
-    # i runs on a copy stream from a device snapshot while step i+1 computes: it is
-    # issued once step i+1's L2 flush has finished, so it overlaps the forward
-    # rather than the flush (whose own time is subtracted); the timed region spans
-    # all steps, from the first upload to the last D2H.
+    # i runs on a copy stream while step i+1 computes: two engines over the same
+    # weights take alternate steps (double-buffered outputs, as a server would
+    # run), so step i's hidden states are read straight from its engine's output
+    # buffer while the other engine computes.  The D2H is issued once step i+1's
+    # L2 flush has finished, so it overlaps the forward rather than the flush
+    # (whose own time is subtracted); the timed region spans all steps, from the
+    # first upload to the last D2H.
+    from paper_2206_01861_b200 import transformer as T
+
+    eng2 = T.EncoderEngine(blocks=eng.blocks, embedding=eng.embedding, final_gamma=eng.final_gamma,
+                           final_beta=eng.final_beta, batch=eng.batch, seq=eng.seq, causal=eng.causal,
+                           lanes=eng.lanes)
+    engs = [eng, eng2]
+    for e_ in engs:  # capture both graphs outside the timed region
+        e_.forward(ids_host)
+    torch.cuda.synchronize()
     out_host = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32).pin_memory() for _ in range(2)]
-    snap = [torch.empty((eng.tokens, BERT["hidden"]), dtype=torch.float32, device="cuda") for _ in range(2)]
+    outs = [None, None]
     copy_stream = torch.cuda.Stream()
     up_stream = torch.cuda.Stream()
     ids_dev = [torch.empty_like(ids_host, device="cuda") for _ in range(2)]
@@ -519,7 +531,7 @@ def run_ours(args, rank: int, world: int, dist):
     def issue_d2h(slot, ready):
         copy_stream.wait_event(ready)
         with torch.cuda.stream(copy_stream):
-            out_host[slot].copy_(snap[slot], non_blocking=True)  # D2H of the result
+            out_host[slot].copy_(outs[slot], non_blocking=True)  # D2H of the result
         copied[slot] = torch.cuda.Event()
         copied[slot].record(copy_stream)
 
@@ -540,14 +552,13 @@ def run_ours(args, rank: int, world: int, dist):
             issue_d2h(*pending)
         j = i % 2
         stream.wait_event(uploaded[j])
-        out = eng.forward(ids_dev[j])        # ids device to device, then the forward graph
+        if copied[j] is not None:
+            stream.wait_event(copied[j])     # the D2H that read this engine's output is done
+        outs[j] = engs[j].forward(ids_dev[j])  # ids device to device, then the forward graph
         consumed[j] = torch.cuda.Event()
         consumed[j].record(stream)
         if i + 1 < args.steps:
             upload((i + 1) % 2)              # the next step's ids, during this forward
-        if copied[j] is not None:
-            stream.wait_event(copied[j])     # the D2H that read snap[j] is done
-        snap[j].copy_(out)
         ready = torch.cuda.Event()
         ready.record(stream)
         pending = (j, ready)
@@ -573,7 +584,7 @@ def run_ours(args, rank: int, world: int, dist):
     clocks = clk.summary()
     step_mm = [1000 * min(step_s), 1000 * max(step_s)]
     ids_bytes, out_bytes = int(ids_host.numel() * 8), int(out_host[0].numel() * 4)
-    del eng, snap, out_host, flush
+    del eng, eng2, engs, outs, out_host, flush
     torch.cuda.empty_cache()
     extra = secondary_workloads(rank, world, dist) if args.workload == "all" else None
     if rank != 0:
@@ -590,7 +601,7 @@ def run_ours(args, rank: int, world: int, dist):
         "config": workload_config(),
         "e2e": {"value": e2e_value, "unit": "seq/s", "h2d_bytes_per_step": ids_bytes,
                 "d2h_bytes_per_step": out_bytes,
-                "pipeline": "D2H of step i overlaps the forward of step i+1 on a copy stream; an L2 flush (256 MiB memset) precedes every step, its own event-timed duration subtracted"},
+                "pipeline": "two engines over the same weights take alternate steps (double-buffered outputs); step i+1's token ids upload on their own stream during step i, and the D2H of step i's hidden states (straight from its engine's output) overlaps step i+1 on a copy stream; an L2 flush (256 MiB memset) precedes every step, its own event-timed duration subtracted"},
         "roofline": roof,
         "row_kernels": rows,
         "cpu_baseline": {"value": cpu_val, "unit": "seq/s", "cores": cores, "kind": "port", "sample": cpu_sample},
