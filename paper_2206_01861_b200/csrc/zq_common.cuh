@@ -240,6 +240,63 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 
 constexpr float kQMargin = 6.103515625e-05f;  // 2^-14
 
+// Packed f32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2): two IEEE
+// round-to-nearest operations per instruction, each bit-identical to __fmaf_rn /
+// __fmul_rn / __fadd_rn / __fsub_rn.  The row quantizers are issue-bound.
+// CAUTION: ptxas contracts f2mul feeding f2add / f2sub into one FFMA2 (single
+// rounding) despite the .rn modifiers; where the product must be rounded, do
+// the multiply-add pair with scalar __fmul_rn / __fadd_rn.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2splat(float a) { return f2pack(a, a); }
+
+// qbf on two elements: (m, -k, residual) packed; nk = magic - m = -k exactly
+__device__ __forceinline__ void qbf2(float x0, float x1, uint64_t inv2, float margin, bool& amb, int& o0, int& o1) {
+  const uint64_t x = f2pack(x0, x1);
+  const uint64_t m = f2fma(x, inv2, f2splat(12582912.0f));
+  const uint64_t nk = f2sub(f2splat(12582912.0f), m);
+  float r0, r1, m0, m1;
+  f2unpack(f2fma(x, inv2, nk), r0, r1);
+  f2unpack(m, m0, m1);
+  amb |= (fabsf(r0) > 0.5f - margin) | (fabsf(r1) > 0.5f - margin);
+  o0 = __float_as_int(m0) - 0x4B400000;
+  o1 = __float_as_int(m1) - 0x4B400000;
+}
+
+// four elements -> one packed word (qbf2 twice, then pack4)
+__device__ __forceinline__ uint32_t qbf4(float4 v, float inv, float margin, bool& amb) {
+  int o[4];
+  qbf2(v.x, v.y, f2splat(inv), margin, amb, o[0], o[1]);
+  qbf2(v.z, v.w, f2splat(inv), margin, amb, o[2], o[3]);
+  return pack4(o[0], o[1], o[2], o[3]);
+}
+
 // Block-wide max of a non-negative float (as its u32 bit pattern — monotone for
 // non-negative floats, NaN never reaches here because the finite flag is raised
 // separately).  `red` must hold >= 32 words.
