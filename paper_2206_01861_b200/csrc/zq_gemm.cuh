@@ -106,10 +106,13 @@ __device__ __forceinline__ void epi_chunk_smem(const uint32_t (&r)[32], float s_
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 w = __ldg(sw4 + j);
-      f[4 * j + 0] = __fmul_rn(__fmul_rn(acc_to_f32<ACCF>(r[4 * j + 0]), s_tok), w.x);
-      f[4 * j + 1] = __fmul_rn(__fmul_rn(acc_to_f32<ACCF>(r[4 * j + 1]), s_tok), w.y);
-      f[4 * j + 2] = __fmul_rn(__fmul_rn(acc_to_f32<ACCF>(r[4 * j + 2]), s_tok), w.z);
-      f[4 * j + 3] = __fmul_rn(__fmul_rn(acc_to_f32<ACCF>(r[4 * j + 3]), s_tok), w.w);
+      // ((acc * s_tok) * s_w) two columns per FMUL2 (the bias add below stays
+      // scalar: ptxas would contract an f32x2 multiply-add into one FFMA2)
+      const uint64_t st2 = f2splat(s_tok);
+      f2unpack(f2mul(f2mul(f2pack(acc_to_f32<ACCF>(r[4 * j + 0]), acc_to_f32<ACCF>(r[4 * j + 1])), st2),
+                     f2pack(w.x, w.y)), f[4 * j + 0], f[4 * j + 1]);
+      f2unpack(f2mul(f2mul(f2pack(acc_to_f32<ACCF>(r[4 * j + 2]), acc_to_f32<ACCF>(r[4 * j + 3])), st2),
+                     f2pack(w.z, w.w)), f[4 * j + 2], f[4 * j + 3]);
     }
     if (bias != nullptr) {
       const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
