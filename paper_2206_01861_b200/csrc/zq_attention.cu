@@ -1834,10 +1834,16 @@ __global__ void __launch_bounds__(QaCfg<CW>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < DPT / 4; ++j) {
       const float4 w = *reinterpret_cast<const float4*>(sw + 4 * j);
-      r[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x));
-      r[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y));
-      r[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z));
-      r[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w));
+      // two columns per FMUL2 (the bias add stays scalar: no f32x2 contraction)
+      float d0, d1, d2, d3;
+      f2unpack(f2mul(f2mul(f2pack(__int2float_rn((int)r[4 * j + 0]), __int2float_rn((int)r[4 * j + 1])), f2splat(s_tok)),
+                     f2pack(w.x, w.y)), d0, d1);
+      f2unpack(f2mul(f2mul(f2pack(__int2float_rn((int)r[4 * j + 2]), __int2float_rn((int)r[4 * j + 3])), f2splat(s_tok)),
+                     f2pack(w.z, w.w)), d2, d3);
+      r[4 * j + 0] = __float_as_uint(d0);
+      r[4 * j + 1] = __float_as_uint(d1);
+      r[4 * j + 2] = __float_as_uint(d2);
+      r[4 * j + 3] = __float_as_uint(d3);
     }
     if (bias != nullptr) {
 #pragma unroll
@@ -2335,10 +2341,16 @@ __global__ void __launch_bounds__(kQsThreads, 1)
 #pragma unroll
       for (int j = 0; j < DPT / 4; ++j) {
         const float4 w = *reinterpret_cast<const float4*>(sw + 4 * j);
-        r[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 0]), s_tok), w.x));
-        r[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 1]), s_tok), w.y));
-        r[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 2]), s_tok), w.z));
-        r[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn(__int2float_rn((int)r[4 * j + 3]), s_tok), w.w));
+        // two columns per FMUL2 (the bias add stays scalar: no f32x2 contraction)
+        float d0, d1, d2, d3;
+        f2unpack(f2mul(f2mul(f2pack(__int2float_rn((int)r[4 * j + 0]), __int2float_rn((int)r[4 * j + 1])), f2splat(s_tok)),
+                       f2pack(w.x, w.y)), d0, d1);
+        f2unpack(f2mul(f2mul(f2pack(__int2float_rn((int)r[4 * j + 2]), __int2float_rn((int)r[4 * j + 3])), f2splat(s_tok)),
+                       f2pack(w.z, w.w)), d2, d3);
+        r[4 * j + 0] = __float_as_uint(d0);
+        r[4 * j + 1] = __float_as_uint(d1);
+        r[4 * j + 2] = __float_as_uint(d2);
+        r[4 * j + 3] = __float_as_uint(d3);
       }
       if (bias != nullptr) {
 #pragma unroll
