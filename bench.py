@@ -889,6 +889,9 @@ def c1_measure(steps: int, warmup: int, rank: int, world: int, out_dtype=None):
     c1_bytes = t * k * 4 + 2 * (t * k + 4 * t) + n * k + 8 * n + t * n * ob
     x_host = torch.randn((t, k)).pin_memory()
     o_host = torch.empty((t, n), dtype=out_dtype).pin_memory()
+    for _ in range(max(warmup, 3)):  # untimed: first-use costs of the eager path and the pinned buffers
+        o_host.copy_(igemm.quantized_linear(x_host.cuda(non_blocking=True), w, bias, igemm.DynamicAct(8),
+                                            out_dtype=out_dtype), non_blocking=True)
     torch.cuda.synchronize()
     ev = []
     for _ in range(steps):
