@@ -366,3 +366,27 @@ def test_quantize_with_absmax_matches_tokenwise(shape):
         if mult == 1.0:
             qa = quant.quantize_activation_tokenwise(xt, 8)
             assert torch.equal(qa.values, q[:, :cols]) and torch.equal(qa.token_scales, s)
+
+
+@pytest.mark.parametrize("t", [300, 16])
+def test_gelu_quantize_far_negative_tail_small_rows(zq, t):
+    """Elements below -5.5 take the estimate at -5.5 (~ -1.04e-7; the reference
+    has |g| <= 1.1e-7 there): they must still quantize to 0, and never decide the
+    row max, for row maxima around the 1e-5 candidate and 3e-5 degenerate-row
+    thresholds; elements just above -5.5 go through the bracket as usual.  300
+    rows: one CTA per row; 16 rows: rows split over a CTA cluster."""
+    _, igemm = zq
+    rng = np.random.default_rng(7 + t)
+    d = 3072
+    x = rng.uniform(-12.0, -5.5, (t, d)).astype(F32)
+    x[:, 7] = -5.5
+    x[:, 8] = np.nextafter(F32(-5.5), F32(0))
+    x[:, 9] = np.nextafter(F32(-5.5), F32(-10))
+    x[:, 10:40] = rng.uniform(-5.5, -4.0, (t, 30)).astype(F32)
+    # the row's only positive element sets the row max: ~GeLU(x) = x / 2 for tiny x
+    peaks = np.array([6.2e-5, 6.0e-5, 5.0e-5, 2.4e-5, 1.0e-5, 2e-6, 1e-3, 0.5], dtype=F32)
+    x[:, 100] = peaks[np.arange(t) % len(peaks)]
+    qa = igemm.gelu_quantize(x, 8)
+    q_ref, s_ref = O.gelu_quantize(x, 8)
+    assert same_bits(h(qa.token_scales), s_ref)
+    assert same_bits(h(qa.values), q_ref)
