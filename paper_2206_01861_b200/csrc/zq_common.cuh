@@ -285,8 +285,10 @@ __device__ __forceinline__ void qbf2(float x0, float x1, uint64_t inv2, float ma
   f2unpack(f2fma(x, inv2, nk), r0, r1);
   f2unpack(m, m0, m1);
   amb |= (fabsf(r0) > 0.5f - margin) | (fabsf(r1) > 0.5f - margin);
-  o0 = __float_as_int(m0) - 0x4B400000;
-  o1 = __float_as_int(m1) - 0x4B400000;
+  // the low byte of 1.5 * 2^23 + k is k's two's-complement byte (0x4B400000 has
+  // a zero low byte and |k| < 2^22): only pack4 / int8 stores consume o0 / o1
+  o0 = __float_as_int(m0);
+  o1 = __float_as_int(m1);
 }
 
 // four elements -> one packed word (qbf2 twice, then pack4)
