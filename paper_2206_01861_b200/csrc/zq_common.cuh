@@ -276,27 +276,21 @@ __device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
 }
 __device__ __forceinline__ uint64_t f2splat(float a) { return f2pack(a, a); }
 
-// qbf on two elements: (m, -k, residual) packed; nk = magic - m = -k exactly
-__device__ __forceinline__ void qbf2(float x0, float x1, uint64_t inv2, float margin, bool& amb, int& o0, int& o1) {
-  const uint64_t x = f2pack(x0, x1);
-  const uint64_t m = f2fma(x, inv2, f2splat(12582912.0f));
-  const uint64_t nk = f2sub(f2splat(12582912.0f), m);
-  float r0, r1, m0, m1;
-  f2unpack(f2fma(x, inv2, nk), r0, r1);
-  f2unpack(m, m0, m1);
-  amb |= (fabsf(r0) > 0.5f - margin) | (fabsf(r1) > 0.5f - margin);
-  // the low byte of 1.5 * 2^23 + k is k's two's-complement byte (0x4B400000 has
-  // a zero low byte and |k| < 2^22): only pack4 / int8 stores consume o0 / o1
-  o0 = __float_as_int(m0);
-  o1 = __float_as_int(m1);
-}
-
-// four elements -> one packed word (qbf2 twice, then pack4)
+// qbf on four elements, two per packed instruction (nk = magic - m = -k exactly;
+// the low byte of m's bits is k's byte, all pack4 reads), one
+// compare on the largest |residual| (FMNMX3; a NaN residual is never ambiguous,
+// as with the per-element compares), then pack4
 __device__ __forceinline__ uint32_t qbf4(float4 v, float inv, float margin, bool& amb) {
-  int o[4];
-  qbf2(v.x, v.y, f2splat(inv), margin, amb, o[0], o[1]);
-  qbf2(v.z, v.w, f2splat(inv), margin, amb, o[2], o[3]);
-  return pack4(o[0], o[1], o[2], o[3]);
+  const uint64_t inv2 = f2splat(inv);
+  const uint64_t xa = f2pack(v.x, v.y), xb = f2pack(v.z, v.w);
+  const uint64_t ma = f2fma(xa, inv2, f2splat(12582912.0f)), mb = f2fma(xb, inv2, f2splat(12582912.0f));
+  float r0, r1, r2, r3, m0, m1, m2, m3;
+  f2unpack(f2fma(xa, inv2, f2sub(f2splat(12582912.0f), ma)), r0, r1);
+  f2unpack(f2fma(xb, inv2, f2sub(f2splat(12582912.0f), mb)), r2, r3);
+  f2unpack(ma, m0, m1);
+  f2unpack(mb, m2, m3);
+  amb |= fmaxf(fmaxf(fabsf(r0), fabsf(r1)), fmaxf(fabsf(r2), fabsf(r3))) > 0.5f - margin;
+  return pack4(__float_as_int(m0), __float_as_int(m1), __float_as_int(m2), __float_as_int(m3));
 }
 
 // Block-wide max of a non-negative float (as its u32 bit pattern — monotone for
