@@ -1,3 +1,8 @@
+# A/B of library builds on one box: LIBS="exp/a.so exp/b.so ..." bash tools/run_ab.sh
+# (alternate the builds, e.g. "a b a b").  Each build is loaded through ZQ_LIB
+# (paper_2206_01861_b200/_native.py) for the row-kernel graph timings and one
+# BERT bench line (value, ms/step, e2e, in-graph row-kernel costs).  Builds go
+# under exp/ (git-ignored, not gpurun-ignored, so they travel to the box).
 for L in $LIBS; do
 echo "== $L"
 ZQ_LIB=$PWD/$L timeout 300 python tools/row_graph_bench.py 2>&1 | grep -v "^$"
